@@ -1,0 +1,192 @@
+/*
+ * hefv.h -- C-ABI of the B200-native RNS/FV hot path (libhefv.so).
+ *
+ * Drop-in boundary for the reference `hepack` FV backend:
+ * every entry point below replaces one CPU routine of the reference, cited
+ * as /root/reference/pkg/src/hepack/<file>:<line>.  Signatures use only
+ * plain pointers, sizes and an opaque context; device pointers are CUDA
+ * global-memory addresses (the Python host side allocates them with torch),
+ * `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *
+ * Conventions
+ *   - A "stack" is (k, N) uint32 residues, limb-major, values in [0, p_j):
+ *     the reference's `np.int64` (k, N) coefficient arrays (fv.py:30-42)
+ *     narrowed to 32 bits.  A ciphertext is (parts, k, N); a batch of B
+ *     ciphertexts is (B, parts, k, N).
+ *   - "device NTT order" is the bit-reversed order of the reference's
+ *     natural evaluation order: dev[i] = NttPrime.fwd(a)[bitrev(i)]
+ *     (ntt.py:145-147).  Switch keys and cached key material live in that
+ *     order, in Montgomery form (x * 2^32 mod p) where noted.
+ *   - Every function returns 0 on success and a negative code on error;
+ *     hefv_last_error() returns a thread-local message.  Launch errors are
+ *     reported synchronously; kernels are asynchronous on `stream`.
+ */
+#ifndef HEFV_H
+#define HEFV_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hefv_ctx hefv_ctx;
+
+/* ---- housekeeping ------------------------------------------------------ */
+const char* hefv_last_error(void);
+int hefv_abi_version(void);
+
+/* Context: NTT tables for a set of word-sized primes (2^28 < p < 2^30) and a
+ * set of 64-bit primes (p < 2^62), ring dimension N = 2^log_n.
+ * Replaces NttPrime.__init__ (ntt.py:149-172) for every prime of
+ * _FvContext.__init__ (fv.py:83, fv.py:95, fv.py:101).  psi is the primitive
+ * 2N-th root the reference picks (g^((p-1)/2N), g the smallest generator). */
+int hefv_ctx_create(hefv_ctx** out, uint32_t log_n, int32_t n32, const uint32_t* primes32,
+                    const uint32_t* psi32, int32_t n64, const uint64_t* primes64,
+                    const uint64_t* psi64);
+void hefv_ctx_destroy(hefv_ctx* ctx);
+
+/* ---- negacyclic NTT (K1/K2/K3) -----------------------------------------
+ * data (batch, nprimes, N); polynomial (b, i) uses prime prime_base + i of
+ * the 32-bit (or 64-bit) set.  natural = 1 uses the reference's natural
+ * evaluation order, 0 the device order.  Inputs of the forward transform
+ * may be any word (reduced mod p on load); inputs of the inverse must be
+ * canonical.  Outputs are canonical.
+ * Replace NttPrime.fwd (ntt.py:216-219) and NttPrime.inv (ntt.py:221-224). */
+int hefv_ntt_fwd32(hefv_ctx* ctx, const uint32_t* in, uint32_t* out, int64_t batch,
+                   int32_t nprimes, int32_t prime_base, int32_t natural, void* stream);
+int hefv_ntt_inv32(hefv_ctx* ctx, const uint32_t* in, uint32_t* out, int64_t batch,
+                   int32_t nprimes, int32_t prime_base, int32_t natural, void* stream);
+int hefv_ntt_fwd64(hefv_ctx* ctx, const uint64_t* in, uint64_t* out, int64_t batch,
+                   int32_t nprimes, int32_t prime_base, int32_t natural, void* stream);
+int hefv_ntt_inv64(hefv_ctx* ctx, const uint64_t* in, uint64_t* out, int64_t batch,
+                   int32_t nprimes, int32_t prime_base, int32_t natural, void* stream);
+
+/* ---- FV layer setup ------------------------------------------------------
+ * k q-primes = 32-bit primes [0, k), a auxiliary primes = [k, k + a),
+ * t = 64-bit prime t_index.  slot_to_ev: (N/2) natural evaluation index of
+ * every slot (fv.py:102-109).  Multiprecision constants are little-endian
+ * 32-bit words: q (wq words), floor(q/2), qhat_i = q/q_i (k x wq),
+ * qhat_inv_i = (q/q_i)^-1 mod q_i; the same for the auxiliary product M
+ * (wm words).  delta_mod_j = floor(q/t) mod q_j (fv.py:86-87). */
+int hefv_fv_setup(hefv_ctx* ctx, int32_t k, int32_t a, int32_t t_index,
+                  const int32_t* slot_to_ev, int32_t wq, const uint32_t* q_words,
+                  const uint32_t* qhalf_words, const uint32_t* qhat_words,
+                  const uint32_t* qhat_inv, int32_t wm, const uint32_t* m_words,
+                  const uint32_t* mhalf_words, const uint32_t* mhat_words,
+                  const uint32_t* mhat_inv, const uint32_t* delta_mod);
+
+/* ---- batching: encode / decode (fv.py:280-289) ---------------------------
+ * slots: (B, N/2) uint64 residues mod t; poly: (B, N) uint64 in [0, t). */
+int hefv_encode(hefv_ctx* ctx, const uint64_t* slots, uint64_t* poly, int64_t B, void* stream);
+int hefv_decode(hefv_ctx* ctx, const uint64_t* poly, uint64_t* slots, int64_t B, void* stream);
+/* Sparse encode for the layer planner: plaintext p has entries
+ * [ptr[p], ptr[p+1]) of (slot, value mod t); others are zero. */
+int hefv_encode_sparse(hefv_ctx* ctx, const int32_t* ptr, const int32_t* slot_idx,
+                       const uint64_t* vals, uint64_t* poly, int64_t P, void* stream);
+
+/* Plaintext poly (B, N) in [0, t) -> RNS stack (B, k, N).
+ * mode 0: Delta * m mod q_j with m uncentred (_delta_m, fv.py:296-310);
+ * mode 1: centred m mod q_j (_centered_plain + `m % tr.p`, fv.py:291-294,
+ *         fv.py:366-370).  to_ntt = 1 additionally applies the forward NTT
+ *         (device order); montgomery = 1 stores x * 2^32 mod q_j. */
+int hefv_plain_to_rns(hefv_ctx* ctx, const uint64_t* poly, uint32_t* out, int64_t B,
+                      int32_t mode, int32_t to_ntt, int32_t montgomery, void* stream);
+
+/* Signed small polynomials (B, N) int8 -> (B, k, N) residues, optionally NTT
+ * (device order) and Montgomery form.  Replaces _FvContext.to_rns (fv.py:119-122). */
+int hefv_small_to_rns(hefv_ctx* ctx, const int8_t* small, uint32_t* out, int64_t B,
+                      int32_t to_ntt, int32_t montgomery, void* stream);
+
+/* ---- elementwise ----------------------------------------------------------
+ * op 0: out = a + b; 1: out = a - b; 2: out = a * b (both canonical, plain
+ * form); 3: out = -(a*b + c) (keygen body); over `rows` stacks of (k, N).
+ * b_rows/c_rows = 1 broadcasts one stack.  Replaces _FvContext.add/neg
+ * (fv.py:131-135) and the pointwise products of fv.py:212-213, 330. */
+int hefv_elementwise(hefv_ctx* ctx, int32_t op, const uint32_t* a, const uint32_t* b,
+                     const uint32_t* c, uint32_t* out, int64_t rows, int64_t b_rows,
+                     int64_t c_rows, void* stream);
+/* out stack = montgomery form of a (x * 2^32 mod p). */
+int hefv_to_montgomery(hefv_ctx* ctx, const uint32_t* a, uint32_t* out, int64_t rows,
+                       void* stream);
+
+/* ---- encryption / decryption (fv.py:317-353) ----------------------------
+ * pk_ntt: (2, k, N) NTT(pk) in device order, Montgomery form.  u, e1, e2:
+ * (B, N) int8 drawn on the host by the reference's Generator calls.  dm:
+ * (B, k, N) Delta*m.  out: (B, 2, k, N). */
+int hefv_encrypt(hefv_ctx* ctx, const uint32_t* pk_ntt, const int8_t* u, const int8_t* e1,
+                 const int8_t* e2, const uint32_t* dm, uint32_t* out, int64_t B, void* stream);
+/* ct: (B, nparts, k, N), nparts in {2, 3}; s_ntt, s2_ntt: (k, N) device
+ * order, Montgomery form.  out: (B, N) uint64 plaintext poly mod t
+ * (decrypt_poly, fv.py:337-349).  scratch: (B, k, N) uint32. */
+int hefv_decrypt(hefv_ctx* ctx, const uint32_t* ct, int32_t nparts, const uint32_t* s_ntt,
+                 const uint32_t* s2_ntt, uint64_t* out, uint32_t* scratch, int64_t B,
+                 void* stream);
+
+/* ---- ciphertext x plaintext (fv.py:364-375) --------------------------------
+ * out[b][part] = iNTT(NTT(ct[b][part]) * m_ntt[b or 0]) for each q prime;
+ * m_ntt: (B or 1, k, N) device order, Montgomery form. */
+int hefv_mul_plain(hefv_ctx* ctx, const uint32_t* ct, const uint32_t* m_ntt, uint32_t* out,
+                   int64_t B, int32_t nparts, int32_t m_broadcast, void* stream);
+/* Layer planner MAC: x_ntt (kin, 2, k, N) Montgomery device-order NTTs of the
+ * input ciphertexts; m_ntt (P, k, N) plain NTTs; row r sums plaintexts
+ * [row_ptr[r], row_ptr[r+1]) each against input ciphertext plain_seg[p];
+ * out (R, 2, k, N) coefficient domain.  Equals the reference's segment
+ * cmult + add chain (inference.py:304-311). */
+int hefv_rows_mac(hefv_ctx* ctx, const uint32_t* x_ntt, const uint32_t* m_ntt,
+                  const int32_t* row_ptr, const int32_t* plain_seg, uint32_t* out, int64_t R,
+                  void* stream);
+
+/* ---- rotations (fv.py:157-173, fv.py:417-432) -----------------------------
+ * Galois automorphism x -> x^g (g odd) of `nparts` parts of B ciphertexts:
+ * source ciphertext b is in + slot[b] * in_stride (slot may be NULL);
+ * out is dense (B, nparts, k, N). */
+int hefv_automorph(hefv_ctx* ctx, const uint32_t* in, int64_t in_stride, const int32_t* slot,
+                   uint32_t* out, int32_t nparts, uint32_t galois_elt, int64_t B, void* stream);
+
+/* RNS-limb key switch (K4, fv.py:205-217), batched over B ciphertexts that
+ * share one switch key.  kbody/kmask: (k, k, N) = [target prime j][digit i],
+ * device NTT order, Montgomery form.  digits of item b: digits + b*dig_stride
+ * ((k, N) coefficient limbs).  Epilogue, per part p in {0,1}:
+ *   out_p[slot b] = d_p + adA_p[b] + adB_p[slot b]     (mod q_j)
+ * with out/adB at ptr + slot[b]*stride (slot may be NULL) and adA dense;
+ * any adA/adB pointer may be NULL; adB may alias out. */
+int hefv_keyswitch(hefv_ctx* ctx, const uint32_t* kbody, const uint32_t* kmask,
+                   const uint32_t* digits, int64_t dig_stride, uint32_t* out0, uint32_t* out1,
+                   int64_t out_stride, const int32_t* slot, const uint32_t* adA0,
+                   const uint32_t* adA1, int64_t adA_stride, const uint32_t* adB0,
+                   const uint32_t* adB1, int64_t adB_stride, int64_t B, void* stream);
+
+/* Switch-key generation for one digit i (fv.py:176-202), NTT domain:
+ *   kbody[j][i] = g_i,j * target[j] - (A_j * s[j] + E_j),  kmask[j][i] = A_j
+ * with A = NTT(a_i), E = NTT(e_i); a_i (k, N) uniform residues, e_i (N) int8;
+ * s_ntt, target_ntt canonical device order; gadget_i: (k) g_i mod q_j.
+ * Outputs are written in Montgomery form. */
+int hefv_keygen_digit(hefv_ctx* ctx, const uint32_t* a_i, const int8_t* e_i, int32_t digit,
+                      const uint32_t* gadget_i, const uint32_t* s_ntt,
+                      const uint32_t* target_ntt, uint32_t* kbody, uint32_t* kmask,
+                      void* stream);
+
+/* ---- ciphertext x ciphertext (K8, fv.py:377-409) --------------------------
+ * Exact BFV tensor with multiprecision CRT lift and t/q rounding.
+ * a, b: (2, k, N) each (b may equal a).  out3: (3, k, N) -- the unrelinearised
+ * parts; scratch: at least 7 * a * N uint32 (aux stacks). */
+int hefv_mult_tensor(hefv_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out3,
+                     uint32_t* scratch, void* stream);
+
+/* ---- layer planner helpers ---------------------------------------------------
+ * out[dst] (+)= sum of rows[r] for r in [seg[m], seg[m+1]) for m < M, with
+ * dst = seg_out[m]; rows (R, 2, k, N); out (nout, 2, k, N).  accumulate = 1
+ * adds into out, 0 overwrites (inference.py:333-338). */
+int hefv_accumulate_rows(hefv_ctx* ctx, const uint32_t* rows, const int32_t* seg,
+                         const int32_t* seg_out, uint32_t* out, int32_t M, int32_t accumulate,
+                         void* stream);
+/* rows[slot[i]] part 0 += add[i] (i < P): the batched add_plain of row biases. */
+int hefv_add_part0(hefv_ctx* ctx, uint32_t* rows, int64_t row_stride, const int32_t* slot,
+                   const uint32_t* add, int64_t P, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HEFV_H */

@@ -1,0 +1,67 @@
+// Internal (C++) view of a context.  Not part of the C-ABI: callers only
+// see the opaque `hefv_ctx*` declared in include/hefv.h.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+#include <cuda_runtime.h>
+
+#include "modarith.cuh"
+
+struct hefv_ctx {
+  int log_n = 0;
+  int n = 0;
+  // word-sized prime set: FV q primes first, then auxiliary primes
+  int n32 = 0;
+  std::vector<uint32_t> primes32;
+  uint2* d_tw32 = nullptr;    // (n32, N) forward twiddles (psi^bitrev, shoup)
+  uint2* d_itw32 = nullptr;   // (n32, N) inverse twiddles
+  hefv::Prime32Info* d_info32 = nullptr;
+  std::vector<hefv::Prime32Info> info32;
+  // 64-bit prime set: plaintext modulus t (FV) or microbench primes
+  int n64 = 0;
+  std::vector<uint64_t> primes64;
+  ulonglong2* d_tw64 = nullptr;
+  ulonglong2* d_itw64 = nullptr;
+  hefv::Prime64Info* d_info64 = nullptr;
+  std::vector<hefv::Prime64Info> info64;
+  // 64-bit Montgomery-free key-switch constants for 64-bit primes
+  // (Shoup companions of keys are built on the fly)
+
+  // ---- FV layer (set by hefv_fv_setup) ----
+  bool fv_ready = false;
+  int k = 0;           // q primes   = primes32[0, k)
+  int a = 0;           // aux primes = primes32[k, k + a)
+  int t_index = 0;     // t = primes64[t_index]
+  uint64_t t = 0;
+  int wq = 0, wm = 0;  // words of q and of the aux product M
+  // device slot maps: slot -> device NTT index, device index -> slot (or -1)
+  int32_t* d_slot_to_dev = nullptr;
+  int32_t* d_dev_to_slot = nullptr;
+  // multiprecision constants (little-endian 32-bit words), device copies
+  uint32_t* d_mp = nullptr;  // one arena, offsets below
+  size_t off_qhat = 0, off_qhatinv = 0, off_q = 0, off_qhalf = 0, off_qnorm = 0;
+  size_t off_mhat = 0, off_mhatinv = 0, off_m = 0, off_mhalf = 0;
+  int q_shift = 0;     // normalisation shift of q for long division
+  uint32_t* d_delta = nullptr;   // Delta mod q_j (k)
+  uint32_t* d_tmod = nullptr;    // t mod q_j (k)
+};
+
+namespace hefv {
+void set_error(const std::string& msg);
+int fail(const std::string& msg);
+int check_cuda(cudaError_t e, const char* where);
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+}  // namespace hefv
+
+#define HEFV_CUDA(call)                                                     \
+  do {                                                                      \
+    cudaError_t _e = (call);                                                \
+    if (_e != cudaSuccess) return hefv::check_cuda(_e, #call);              \
+  } while (0)
+
+#define HEFV_LAUNCH_CHECK(where)                                            \
+  do {                                                                      \
+    cudaError_t _e = cudaGetLastError();                                    \
+    if (_e != cudaSuccess) return hefv::check_cuda(_e, where);              \
+  } while (0)

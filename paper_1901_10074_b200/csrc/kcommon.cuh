@@ -1,0 +1,36 @@
+// Small device helpers shared by the kernel translation units.
+#pragma once
+#include "modarith.cuh"
+
+namespace hefv {
+
+__device__ __forceinline__ Mod32 make_mod(const Prime32Info& i) { return Mod32{i.p, 2 * i.p}; }
+__device__ __forceinline__ Mod64 make_mod(const Prime64Info& i) { return Mod64{i.p, 2 * i.p}; }
+__device__ __forceinline__ uint32_t reduce_any(uint32_t x, const Prime32Info& i) {
+  return barrett62(x, i.p, i.mu);
+}
+__device__ __forceinline__ uint64_t reduce_any(uint64_t x, const Prime64Info& i) {
+  return x >= i.p ? x % i.p : x;
+}
+
+template <class M>
+struct InfoOf;
+template <>
+struct InfoOf<Mod32> {
+  typedef Prime32Info I;
+};
+template <>
+struct InfoOf<Mod64> {
+  typedef Prime64Info I;
+};
+
+__device__ __forceinline__ int brev_n(int x, int logn) { return (int)(__brev((unsigned)x) >> (32 - logn)); }
+
+
+// LOGE (log2 words per thread) used by the CTA-resident 32-bit transforms.
+template <int LOGN>
+struct Loge32 {
+  static constexpr int v = LOGN >= 15 ? 5 : 4;
+};
+
+}  // namespace hefv

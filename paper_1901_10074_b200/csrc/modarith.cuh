@@ -1,0 +1,131 @@
+// Modular arithmetic primitives for the RNS/FV hot path (sm_100a).
+//
+// Two word sizes:
+//   * Mod32 -- the FV q / auxiliary primes (30-bit, 2^28 < p < 2^30, see
+//     fv.py:60-64 and fv.py:89-95 of the reference: `find_ntt_primes(count,
+//     30, 2n)`).  Twiddle products use Shoup's trick with a 32-bit companion
+//     (the same constant family as ntt.py:166-170), key products use
+//     Montgomery REDC so the switch keys stay at one word per coefficient.
+//   * Mod64 -- the plaintext modulus t (18..53 bits at the shipped profiles)
+//     and the 50-62-bit primes of the kernel microbench (config 4).  Shoup
+//     with a 64-bit companion; requires p < 2^62 so lazy values < 4p fit.
+//
+// All butterflies are Harvey-style lazy: forward (Cooley-Tukey) keeps
+// values in [0, 4p), inverse (Gentleman-Sande) in [0, 2p).  Results leave a
+// kernel only after the final correction to the canonical range [0, p), so
+// every limb that reaches HBM is bit-identical to the reference's
+// canonical residues.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hefv {
+
+// ---------------------------------------------------------------- 32-bit
+struct Mod32 {
+  typedef uint32_t T;
+  typedef uint2 Tw;  // (w, floor(w * 2^32 / p))
+  uint32_t p, p2;
+
+  __device__ __forceinline__ static uint32_t mul_shoup(uint32_t x, uint32_t w, uint32_t wsh,
+                                                       uint32_t p) {
+    uint32_t q = __umulhi(x, wsh);
+    return x * w - q * p;  // in [0, 2p) for any x < 2^32
+  }
+  __device__ __forceinline__ uint32_t sub2p(uint32_t x) const { return min(x, x - p2); }
+  __device__ __forceinline__ uint32_t subp(uint32_t x) const { return min(x, x - p); }
+  // canonical from [0, 4p)
+  __device__ __forceinline__ uint32_t canon4(uint32_t x) const { return subp(sub2p(x)); }
+  __device__ __forceinline__ void ct(uint32_t& x, uint32_t& y, Tw w) const {
+    uint32_t a = sub2p(x);
+    uint32_t t = mul_shoup(y, w.x, w.y, p);
+    x = a + t;
+    y = a - t + p2;
+  }
+  __device__ __forceinline__ void gs(uint32_t& x, uint32_t& y, Tw w) const {
+    uint32_t a = x, b = y;
+    x = sub2p(a + b);
+    y = mul_shoup(a - b + p2, w.x, w.y, p);
+  }
+  // last inverse stage with N^{-1} merged: x' = (a+b) n^-1, y' = (a-b) w n^-1
+  __device__ __forceinline__ void gs_last(uint32_t& x, uint32_t& y, Tw ninv, Tw wn) const {
+    uint32_t a = x, b = y;
+    x = mul_shoup(a + b, ninv.x, ninv.y, p);
+    y = mul_shoup(a - b + p2, wn.x, wn.y, p);
+  }
+};
+
+// Montgomery REDC for a*b with b < p and a < 2^32: returns a*b*2^-32 mod p in [0, 2p).
+__device__ __forceinline__ uint32_t mont_mul_lazy(uint32_t a, uint32_t b, uint32_t p,
+                                                  uint32_t pinv_neg) {
+  uint64_t t = (uint64_t)a * b;
+  uint32_t lo = (uint32_t)t;
+  uint32_t m = lo * pinv_neg;
+  uint32_t h = __umulhi(m, p);
+  return (uint32_t)(t >> 32) + h + (lo != 0u);
+}
+
+// ---------------------------------------------------------------- 64-bit
+struct Mod64 {
+  typedef uint64_t T;
+  typedef ulonglong2 Tw;  // (w, floor(w * 2^64 / p))
+  uint64_t p, p2;
+
+  __device__ __forceinline__ static uint64_t mul_shoup(uint64_t x, uint64_t w, uint64_t wsh,
+                                                       uint64_t p) {
+    uint64_t q = __umul64hi(x, wsh);
+    return x * w - q * p;  // in [0, 2p)
+  }
+  __device__ __forceinline__ uint64_t sub2p(uint64_t x) const { return x >= p2 ? x - p2 : x; }
+  __device__ __forceinline__ uint64_t subp(uint64_t x) const { return x >= p ? x - p : x; }
+  __device__ __forceinline__ uint64_t canon4(uint64_t x) const { return subp(sub2p(x)); }
+  __device__ __forceinline__ void ct(uint64_t& x, uint64_t& y, Tw w) const {
+    uint64_t a = sub2p(x);
+    uint64_t t = mul_shoup(y, w.x, w.y, p);
+    x = a + t;
+    y = a - t + p2;
+  }
+  __device__ __forceinline__ void gs(uint64_t& x, uint64_t& y, Tw w) const {
+    uint64_t a = x, b = y;
+    x = sub2p(a + b);
+    y = mul_shoup(a - b + p2, w.x, w.y, p);
+  }
+  __device__ __forceinline__ void gs_last(uint64_t& x, uint64_t& y, Tw ninv, Tw wn) const {
+    uint64_t a = x, b = y;
+    x = mul_shoup(a + b, ninv.x, ninv.y, p);
+    y = mul_shoup(a - b + p2, wn.x, wn.y, p);
+  }
+};
+
+// Full 64x64 -> mod p product for p < 2^62 (variable x variable); used off the
+// transform path (pointwise products of 64-bit residues).
+__device__ __forceinline__ uint64_t mulmod64(uint64_t a, uint64_t b, uint64_t p) {
+  unsigned __int128 t = (unsigned __int128)a * b;
+  return (uint64_t)(t % p);
+}
+
+// Barrett reduction of x < 2^62 by a 30-bit prime with mu = floor(2^64 / p).
+__device__ __forceinline__ uint32_t barrett62(uint64_t x, uint32_t p, uint64_t mu) {
+  uint64_t q = __umul64hi(x, mu);
+  uint64_t r = x - q * p;
+  return (uint32_t)(r >= p ? r - p : r);
+}
+
+// Per-prime constants (one record per 32-bit prime of a context).
+struct Prime32Info {
+  uint32_t p;
+  uint32_t pinv_neg;  // -p^{-1} mod 2^32
+  uint32_t r2;        // 2^64 mod p (to enter Montgomery form)
+  uint32_t pad;
+  uint64_t mu;        // floor(2^64 / p)
+  uint2 ninv;         // (N^{-1}, shoup)
+  uint2 wn;           // (psi_inv_rev[1] * N^{-1}, shoup)
+};
+
+struct Prime64Info {
+  uint64_t p;
+  ulonglong2 ninv;
+  ulonglong2 wn;
+};
+
+}  // namespace hefv

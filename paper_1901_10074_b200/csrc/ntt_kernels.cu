@@ -1,0 +1,368 @@
+// Standalone batched negacyclic NTTs (K1/K2 for 30-bit primes, K3 for
+// 64-bit primes): one CTA per polynomial, the polynomial resident in
+// registers + one padded shared tile (ntt.cuh).  Replaces NttPrime.fwd/inv
+// (reference ntt.py:191-224) including the object-dtype path for p >= 2^31.
+//
+// For 64-bit primes with N > 2^14 the polynomial (>= 256 KB) does not fit a
+// CTA's shared memory; those sizes run the two-kernel global-memory variant
+// at the end of this file (column pass + row pass, each CTA-resident).
+#include "../../include/hefv.h"
+#include "internal.h"
+#include "ntt.cuh"
+#include "kcommon.cuh"
+
+namespace hefv {
+
+template <int LOGN, int LOGE, class M>
+__global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT)
+    k_ntt_fwd(const typename M::T* __restrict__ in, typename M::T* __restrict__ out, int nprimes,
+              int prime_base, int natural, const typename M::Tw* __restrict__ tw_all,
+              const typename InfoOf<M>::I* __restrict__ info) {
+  typedef Geo<LOGN, LOGE> G_;
+  typedef typename M::T T;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T* sm = reinterpret_cast<T*>(smraw);
+  const size_t poly = blockIdx.x;
+  const int pi = prime_base + (int)(poly % nprimes);
+  const auto inf = info[pi];
+  const M md = make_mod(inf);
+  const typename M::Tw* tw = tw_all + (size_t)pi * G_::N;
+  const T* src = in + poly * G_::N;
+  T* dst = out + poly * G_::N;
+  const int tid = threadIdx.x;
+  T x[G_::E];
+#pragma unroll
+  for (int e = 0; e < G_::E; ++e) x[e] = reduce_any(src[tid + e * G_::NT], inf);
+  cta_fwd<LOGN, LOGE, M>(md, x, sm, tw);
+#pragma unroll
+  for (int e = 0; e < G_::E; ++e) x[e] = md.canon4(x[e]);
+  if (!natural) {
+#pragma unroll
+    for (int e = 0; e < G_::E; ++e) dst[tid * G_::E + e] = x[e];
+  } else {
+    // dev index i holds natural index bitrev(i): stage through smem
+#pragma unroll
+    for (int e = 0; e < G_::E; ++e) sm[spad(brev_n(tid * G_::E + e, LOGN))] = x[e];
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < G_::E; ++e) dst[tid + e * G_::NT] = sm[spad(tid + e * G_::NT)];
+  }
+}
+
+template <int LOGN, int LOGE, class M>
+__global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT)
+    k_ntt_inv(const typename M::T* __restrict__ in, typename M::T* __restrict__ out, int nprimes,
+              int prime_base, int natural, const typename M::Tw* __restrict__ itw_all,
+              const typename InfoOf<M>::I* __restrict__ info) {
+  typedef Geo<LOGN, LOGE> G_;
+  typedef typename M::T T;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T* sm = reinterpret_cast<T*>(smraw);
+  const size_t poly = blockIdx.x;
+  const int pi = prime_base + (int)(poly % nprimes);
+  const auto inf = info[pi];
+  const M md = make_mod(inf);
+  const typename M::Tw* itw = itw_all + (size_t)pi * G_::N;
+  const T* src = in + poly * G_::N;
+  T* dst = out + poly * G_::N;
+  const int tid = threadIdx.x;
+  T x[G_::E];
+  if (!natural) {
+#pragma unroll
+    for (int e = 0; e < G_::E; ++e) x[e] = src[tid * G_::E + e];
+  } else {
+#pragma unroll
+    for (int e = 0; e < G_::E; ++e)
+      sm[spad(brev_n(tid + e * G_::NT, LOGN))] = src[tid + e * G_::NT];
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < G_::E; ++e) x[e] = sm[spad(tid * G_::E + e)];
+    __syncthreads();
+  }
+  cta_inv<LOGN, LOGE, M>(md, x, sm, itw, inf.ninv, inf.wn);
+#pragma unroll
+  for (int e = 0; e < G_::E; ++e) dst[tid + e * G_::NT] = md.subp(x[e]);
+}
+
+template <int LOGN, int LOGE, class M>
+static int launch_one(bool fwd, const typename M::T* in, typename M::T* out, int64_t batch,
+                      int nprimes, int prime_base, int natural, const typename M::Tw* tw,
+                      const typename InfoOf<M>::I* info, cudaStream_t st) {
+  typedef Geo<LOGN, LOGE> G_;
+  const size_t smem = (size_t)spad_size(G_::N) * sizeof(typename M::T);
+  const int64_t total = batch * nprimes;
+  if (total <= 0) return 0;
+  if (total > 0x7fffffff) return fail("ntt: batch too large");
+  if (fwd) {
+    auto kern = k_ntt_fwd<LOGN, LOGE, M>;
+    HEFV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)total, G_::NT, smem, st>>>(in, out, nprimes, prime_base, natural, tw, info);
+  } else {
+    auto kern = k_ntt_inv<LOGN, LOGE, M>;
+    HEFV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)total, G_::NT, smem, st>>>(in, out, nprimes, prime_base, natural, tw, info);
+  }
+  HEFV_LAUNCH_CHECK("ntt kernel launch");
+  return 0;
+}
+
+template <class M>
+static int dispatch(int log_n, bool fwd, const typename M::T* in, typename M::T* out,
+                    int64_t batch, int nprimes, int prime_base, int natural,
+                    const typename M::Tw* tw, const typename InfoOf<M>::I* info, cudaStream_t st) {
+#define HEFV_CASE(L) \
+  case L:            \
+    return launch_one<L, 4, M>(fwd, in, out, batch, nprimes, prime_base, natural, tw, info, st);
+  switch (log_n) {
+    HEFV_CASE(4)
+    HEFV_CASE(5)
+    HEFV_CASE(6)
+    HEFV_CASE(7)
+    HEFV_CASE(8)
+    HEFV_CASE(9)
+    HEFV_CASE(10)
+    HEFV_CASE(11)
+    HEFV_CASE(12)
+    HEFV_CASE(13)
+    HEFV_CASE(14)
+    default:
+      break;
+  }
+#undef HEFV_CASE
+  if constexpr (sizeof(typename M::T) == 4) {
+    if (log_n == 15)
+      return launch_one<15, 5, M>(fwd, in, out, batch, nprimes, prime_base, natural, tw, info, st);
+  }
+  return -100;  // not handled by the CTA-resident path
+}
+
+}  // namespace hefv
+
+using namespace hefv;
+
+int hefv_ntt64_large(hefv_ctx* c, bool fwd, const uint64_t* in, uint64_t* out, int64_t batch,
+                     int nprimes, int prime_base, int natural, cudaStream_t st);
+
+extern "C" {
+
+int hefv_ntt_fwd32(hefv_ctx* c, const uint32_t* in, uint32_t* out, int64_t batch,
+                   int32_t nprimes, int32_t prime_base, int32_t natural, void* stream) {
+  if (!c) return fail("ntt_fwd32: null context");
+  if (nprimes < 1 || prime_base < 0 || prime_base + nprimes > c->n32)
+    return fail("ntt_fwd32: prime range outside the context");
+  int r = dispatch<Mod32>(c->log_n, true, in, out, batch, nprimes, prime_base, natural, c->d_tw32,
+                          c->d_info32, as_stream(stream));
+  if (r == -100) return fail("ntt_fwd32: N = 2^16 is not supported for 32-bit primes");
+  return r;
+}
+
+int hefv_ntt_inv32(hefv_ctx* c, const uint32_t* in, uint32_t* out, int64_t batch,
+                   int32_t nprimes, int32_t prime_base, int32_t natural, void* stream) {
+  if (!c) return fail("ntt_inv32: null context");
+  if (nprimes < 1 || prime_base < 0 || prime_base + nprimes > c->n32)
+    return fail("ntt_inv32: prime range outside the context");
+  int r = dispatch<Mod32>(c->log_n, false, in, out, batch, nprimes, prime_base, natural,
+                          c->d_itw32, c->d_info32, as_stream(stream));
+  if (r == -100) return fail("ntt_inv32: N = 2^16 is not supported for 32-bit primes");
+  return r;
+}
+
+int hefv_ntt_fwd64(hefv_ctx* c, const uint64_t* in, uint64_t* out, int64_t batch,
+                   int32_t nprimes, int32_t prime_base, int32_t natural, void* stream) {
+  if (!c) return fail("ntt_fwd64: null context");
+  if (nprimes < 1 || prime_base < 0 || prime_base + nprimes > c->n64)
+    return fail("ntt_fwd64: prime range outside the context");
+  int r = dispatch<Mod64>(c->log_n, true, in, out, batch, nprimes, prime_base, natural, c->d_tw64,
+                          c->d_info64, as_stream(stream));
+  if (r == -100)
+    return hefv_ntt64_large(c, true, in, out, batch, nprimes, prime_base, natural,
+                            as_stream(stream));
+  return r;
+}
+
+int hefv_ntt_inv64(hefv_ctx* c, const uint64_t* in, uint64_t* out, int64_t batch,
+                   int32_t nprimes, int32_t prime_base, int32_t natural, void* stream) {
+  if (!c) return fail("ntt_inv64: null context");
+  if (nprimes < 1 || prime_base < 0 || prime_base + nprimes > c->n64)
+    return fail("ntt_inv64: prime range outside the context");
+  int r = dispatch<Mod64>(c->log_n, false, in, out, batch, nprimes, prime_base, natural,
+                          c->d_itw64, c->d_info64, as_stream(stream));
+  if (r == -100)
+    return hefv_ntt64_large(c, false, in, out, batch, nprimes, prime_base, natural,
+                            as_stream(stream));
+  return r;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// 64-bit primes, N in {2^15, 2^16}: two CTA-resident passes through HBM.
+// Pass A (stages [0, S)) treats the polynomial as 2^S columns-interleaved
+// sub-problems: CTA c handles the 2^S elements {c' + e * (N >> S)} for a
+// group of consecutive columns; pass B (stages [S, LOGN)) handles contiguous
+// blocks of N >> S elements.  Both passes use the same twiddle indexing as
+// the single-CTA transform, so results are identical.
+// ---------------------------------------------------------------------------
+namespace hefv {
+
+// Pass over stages [s0, s0 + R) of a length-N transform for blocks of 2^R
+// elements with element stride T = N >> (s0 + R).  One thread per block.
+template <int R, bool FWD>
+__global__ void __launch_bounds__(256)
+    k_ntt64_radix_pass(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, int log_n,
+                       int s0, int nprimes, int prime_base, int64_t nblocks_per_poly,
+                       int64_t total_blocks, const ulonglong2* __restrict__ tw_all,
+                       const Prime64Info* __restrict__ info, int last_inverse, int canon_out) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= total_blocks) return;
+  const int64_t poly = gid / nblocks_per_poly;
+  const int64_t blk = gid % nblocks_per_poly;
+  const int n = 1 << log_n;
+  const int pi = prime_base + (int)(poly % nprimes);
+  const Prime64Info inf = info[pi];
+  const Mod64 md{inf.p, 2 * inf.p};
+  const ulonglong2* tw = tw_all + (size_t)pi * n;
+  const int tsh = log_n - s0 - R;
+  const int64_t L = blk & ((1ll << tsh) - 1);
+  const int64_t G = blk >> tsh;
+  const int64_t base = (G << (log_n - s0)) + L;
+  const uint64_t* src = in + poly * n;
+  uint64_t* dst = out + poly * n;
+  uint64_t x[1 << R];
+#pragma unroll
+  for (int e = 0; e < (1 << R); ++e) x[e] = src[base + ((int64_t)e << tsh)];
+  if (FWD) {
+    if (s0 == 0) {
+#pragma unroll
+      for (int e = 0; e < (1 << R); ++e) x[e] = reduce_any(x[e], inf);
+    }
+#pragma unroll
+    for (int l = 0; l < R; ++l) {
+      const int half = (1 << R) >> (l + 1);
+      const ulonglong2* twb = tw + (1ll << (s0 + l)) + (G << l);
+#pragma unroll
+      for (int u = 0; u < (1 << l); ++u) {
+        const ulonglong2 w = twb[u];
+#pragma unroll
+        for (int e0 = 0; e0 < half; ++e0) {
+          const int e = u * 2 * half + e0;
+          md.ct(x[e], x[e + half], w);
+        }
+      }
+    }
+    if (canon_out) {
+#pragma unroll
+      for (int e = 0; e < (1 << R); ++e) x[e] = md.canon4(x[e]);
+    }
+  } else {
+#pragma unroll
+    for (int l = R - 1; l >= 0; --l) {
+      const int half = (1 << R) >> (l + 1);
+      const ulonglong2* twb = tw + (1ll << (s0 + l)) + (G << l);
+#pragma unroll
+      for (int u = 0; u < (1 << l); ++u) {
+#pragma unroll
+        for (int e0 = 0; e0 < half; ++e0) {
+          const int e = u * 2 * half + e0;
+          if (last_inverse && s0 + l == 0)
+            md.gs_last(x[e], x[e + half], inf.ninv, inf.wn);
+          else
+            md.gs(x[e], x[e + half], twb[u]);
+        }
+      }
+    }
+    if (canon_out) {
+#pragma unroll
+      for (int e = 0; e < (1 << R); ++e) x[e] = md.subp(x[e]);
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < (1 << R); ++e) dst[base + ((int64_t)e << tsh)] = x[e];
+}
+
+__global__ void k_permute_bitrev64(const uint64_t* __restrict__ in, uint64_t* __restrict__ out,
+                                   int log_n, int64_t total) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= total) return;
+  const int64_t n = 1ll << log_n;
+  const int64_t poly = gid >> log_n;
+  const int i = (int)(gid & (n - 1));
+  out[poly * n + brev_n(i, log_n)] = in[gid];
+}
+
+}  // namespace hefv
+
+int hefv_ntt64_large(hefv_ctx* c, bool fwd, const uint64_t* in, uint64_t* out, int64_t batch,
+                     int nprimes, int prime_base, int natural, cudaStream_t st) {
+  const int log_n = c->log_n;
+  const int64_t n = c->n;
+  const int64_t total_polys = batch * nprimes;
+  if (total_polys <= 0) return 0;
+  // radix-16 passes: stages in groups of 4 (log_n = 15 -> 4,4,4,3; 16 -> 4,4,4,4)
+  const int64_t blocks16 = n / 16;
+  const int threads = 256;
+  auto grid_for = [&](int64_t nb) { return (unsigned)((nb * total_polys + threads - 1) / threads); };
+  // the transform runs in place in `out`; the first pass reads `in`
+  const uint64_t* src = in;
+  if (fwd) {
+    int s0 = 0;
+    while (s0 < log_n) {
+      const int r = (log_n - s0) >= 4 ? 4 : (log_n - s0);
+      const bool last = s0 + r == log_n;
+      const int64_t nb = n >> r;
+      if (r == 4)
+        k_ntt64_radix_pass<4, true><<<grid_for(nb), threads, 0, st>>>(
+            src, out, log_n, s0, nprimes, prime_base, nb, nb * total_polys, c->d_tw64, c->d_info64,
+            0, last ? 1 : 0);
+      else
+        k_ntt64_radix_pass<3, true><<<grid_for(nb), threads, 0, st>>>(
+            src, out, log_n, s0, nprimes, prime_base, nb, nb * total_polys, c->d_tw64, c->d_info64,
+            0, last ? 1 : 0);
+      HEFV_LAUNCH_CHECK("ntt64 large pass");
+      src = out;
+      s0 += r;
+    }
+    if (natural) {
+      // out holds device order; permute into a temporary then copy back
+      uint64_t* tmp = nullptr;
+      HEFV_CUDA(cudaMallocAsync(&tmp, total_polys * n * 8, st));
+      const int64_t tot = total_polys * n;
+      k_permute_bitrev64<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(out, tmp, log_n, tot);
+      HEFV_LAUNCH_CHECK("ntt64 permute");
+      HEFV_CUDA(cudaMemcpyAsync(out, tmp, tot * 8, cudaMemcpyDeviceToDevice, st));
+      HEFV_CUDA(cudaFreeAsync(tmp, st));
+    }
+  } else {
+    if (natural) {
+      const int64_t tot = total_polys * n;
+      k_permute_bitrev64<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(in, out, log_n, tot);
+      HEFV_LAUNCH_CHECK("ntt64 permute");
+      src = out;
+    }
+    // inverse: stages from log_n - 1 down to 0, passes in reverse grouping
+    std::vector<std::pair<int, int>> passes;  // (s0, r)
+    int s0 = 0;
+    while (s0 < log_n) {
+      const int r = (log_n - s0) >= 4 ? 4 : (log_n - s0);
+      passes.push_back({s0, r});
+      s0 += r;
+    }
+    for (int pi = (int)passes.size() - 1; pi >= 0; --pi) {
+      const int ps = passes[pi].first, r = passes[pi].second;
+      const int64_t nb = n >> r;
+      const bool last = ps == 0;
+      if (r == 4)
+        k_ntt64_radix_pass<4, false><<<grid_for(nb), threads, 0, st>>>(
+            src, out, log_n, ps, nprimes, prime_base, nb, nb * total_polys, c->d_itw64,
+            c->d_info64, 1, last ? 1 : 0);
+      else
+        k_ntt64_radix_pass<3, false><<<grid_for(nb), threads, 0, st>>>(
+            src, out, log_n, ps, nprimes, prime_base, nb, nb * total_polys, c->d_itw64,
+            c->d_info64, 1, last ? 1 : 0);
+      HEFV_LAUNCH_CHECK("ntt64 large pass");
+      src = out;
+    }
+  }
+  (void)blocks16;
+  return 0;
+}

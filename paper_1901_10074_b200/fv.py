@@ -1,0 +1,671 @@
+"""Fan-Vercauteren over RNS, device-resident: the GPU drop-in for the
+reference's ``hepack.fv`` (/root/reference/pkg/src/hepack/fv.py).
+
+Same public surface -- ``FvParams``, ``SwitchKey``, ``KeySet``, ``keygen``,
+``FvCiphertext``, ``FvBackend``, ``run_sequence``, ``fv_conformance`` -- and
+bit-identical results: keys and encryption randomness are drawn on the host
+through the caller's ``numpy.random.Generator`` with exactly the reference's
+calls and order (fv.py:114-129, 231-251, 317-321); everything else (NTTs,
+key generation arithmetic, encryption, decryption rounding, ct x pt, exact
+ct x ct tensor + relinearisation, Galois key switching) runs in libhefv.so.
+
+Ciphertexts live in HBM as (parts, k, N) uint32 stacks; ``FvCiphertext.parts``
+downloads lazily to the reference's list of (k, N) int64 arrays.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as nat
+from .engine import SlotBackend
+from .errors import ParamMismatchError
+from .params import BackendParams
+from .ring import (
+    WORD_BITS,
+    CrtConstants,
+    bitrev_perm,
+    find_ntt_primes,
+    gadget,
+    galois_element,
+    root_of_unity,
+    slot_to_eval,
+)
+
+SIGMA = 3.2
+ERR_BOUND = 19  # 6-sigma truncation (fv.py:25-26)
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+# ---------------------------------------------------------------------------
+# parameters
+# ---------------------------------------------------------------------------
+@dataclass
+class FvParams:
+    """n, t and the q primes (fv.py:45-64)."""
+
+    n: int
+    t: int
+    q_primes: list
+    sigma: float = SIGMA
+
+    def __post_init__(self):
+        if self.t % (2 * self.n) != 1:
+            raise ValueError(
+                f"plain_modulus {self.t} must be 1 mod 2n={2 * self.n} for batching")
+
+    @classmethod
+    def from_backend(cls, params: BackendParams) -> "FvParams":
+        count = max(2, -(-params.coeff_modulus_bits // WORD_BITS))
+        primes = find_ntt_primes(count, WORD_BITS, 2 * params.ring_dimension)
+        return cls(n=params.ring_dimension, t=params.plain_modulus, q_primes=primes)
+
+
+# ---------------------------------------------------------------------------
+# device context
+# ---------------------------------------------------------------------------
+class FvContext:
+    """Constants of one parameter set, mirrored on the device.
+
+    Host attributes follow _FvContext (fv.py:75-110): n, t, q, delta,
+    delta_mod, aux_primes, gadget, slot_to_ev, fp.  ``q_ntt``/``aux_ntt``/
+    ``t_ntt`` are GPU ``NttPrime`` objects created on first use."""
+
+    def __init__(self, fp: FvParams):
+        import ctypes as C
+
+        nat.require_device()
+        lib = nat.load()
+        torch = _torch()
+        self.fp = fp
+        self.n = n = fp.n
+        self.log_n = n.bit_length() - 1
+        if self.log_n > 14:
+            raise ValueError("the FV kernels support ring dimensions up to 2^14")
+        self.t = fp.t
+        self.q_primes = list(fp.q_primes)
+        self.k = len(self.q_primes)
+        qc = CrtConstants.build(self.q_primes)
+        self.q = qc.product
+        self.delta = self.q // fp.t
+        self.delta_mod = [self.delta % p for p in self.q_primes]
+        need_bits = n.bit_length() + 2 * self.q.bit_length() + 2
+        count = -(-need_bits // (WORD_BITS - 1))
+        self.aux_primes = find_ntt_primes(count, WORD_BITS, 2 * n, below=min(self.q_primes))
+        self.a = len(self.aux_primes)
+        mc = CrtConstants.build(self.aux_primes)
+        self.gadget = gadget(self.q_primes)
+        self.slot_to_ev = slot_to_eval(n)
+        if fp.t >= 1 << 62:
+            raise ValueError("plain modulus must be below 2^62")
+        primes32 = self.q_primes + self.aux_primes
+        psi32 = [root_of_unity(p, n) for p in primes32]
+        psi_t = root_of_unity(fp.t, n)
+        arr32 = (C.c_uint32 * len(primes32))(*primes32)
+        apsi32 = (C.c_uint32 * len(primes32))(*psi32)
+        arr64 = (C.c_uint64 * 1)(fp.t)
+        apsi64 = (C.c_uint64 * 1)(psi_t)
+        h = C.c_void_p()
+        nat.check(lib.hefv_ctx_create(C.byref(h), self.log_n, len(primes32), arr32, apsi32, 1,
+                                      arr64, apsi64), "hefv_ctx_create")
+        self._h = h
+        self._lib = lib
+
+        def cbuf(a, ctype):
+            a = np.ascontiguousarray(a)
+            return a.ctypes.data_as(C.POINTER(ctype)), a
+
+        keep = []
+
+        def c32(a):
+            p, arr = cbuf(np.asarray(a, dtype=np.uint32), C.c_uint32)
+            keep.append(arr)
+            return p
+
+        s2e = np.ascontiguousarray(self.slot_to_ev.astype(np.int32))
+        keep.append(s2e)
+        nat.check(lib.hefv_fv_setup(
+            h, self.k, self.a, 0, s2e.ctypes.data_as(C.POINTER(C.c_int32)),
+            qc.words, c32(qc.prod_words), c32(qc.half_words), c32(qc.hat_words.reshape(-1)),
+            c32(qc.hat_inv), mc.words, c32(mc.prod_words), c32(mc.half_words),
+            c32(mc.hat_words.reshape(-1)), c32(mc.hat_inv), c32(self.delta_mod)),
+            "hefv_fv_setup")
+        # gadget_i mod q_j table (k x k)
+        gtab = np.array([[g % p for p in self.q_primes] for g in self.gadget], dtype=np.int64)
+        self.d_gadget = torch.from_numpy(gtab.astype(np.int32)).cuda()
+        self.p_col = np.array(self.q_primes, dtype=np.int64)[:, None]
+        self.brev = bitrev_perm(self.log_n)
+        self._ntt_cache = {}
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and nat._lib is not None:
+            nat._lib.hefv_ctx_destroy(h)
+            self._h = None
+
+    # ---- reference-compatible transform objects (lazy) ----
+    def _ntt(self, p):
+        from .ntt import NttPrime
+
+        tr = self._ntt_cache.get(p)
+        if tr is None:
+            tr = self._ntt_cache[p] = NttPrime(p, self.n)
+        return tr
+
+    @property
+    def q_ntt(self):
+        return [self._ntt(p) for p in self.q_primes]
+
+    @property
+    def aux_ntt(self):
+        return [self._ntt(p) for p in self.aux_primes]
+
+    @property
+    def t_ntt(self):
+        return self._ntt(self.t)
+
+    # ---- host samplers: identical Generator calls (fv.py:114-129) ----
+    def rand_uniform(self, rng) -> np.ndarray:
+        return np.stack([rng.integers(0, p, self.n, dtype=np.int64) for p in self.q_primes])
+
+    def rand_ternary(self, rng) -> np.ndarray:
+        return rng.integers(-1, 2, self.n, dtype=np.int64)
+
+    def rand_error(self, rng) -> np.ndarray:
+        e = np.rint(rng.normal(0.0, self.fp.sigma, self.n)).astype(np.int64)
+        return np.clip(e, -ERR_BOUND, ERR_BOUND)
+
+    def to_rns(self, small) -> np.ndarray:
+        return np.asarray(small, dtype=np.int64) % self.p_col
+
+    def galois_small(self, small: np.ndarray, g: int) -> np.ndarray:
+        """x -> x^g on a small signed host polynomial (fv.py:157-173)."""
+        j = np.arange(self.n, dtype=np.int64)
+        idx = j * g % (2 * self.n)
+        out = np.zeros(self.n, dtype=np.int64)
+        out[idx % self.n] = np.where(idx < self.n, small, -small)
+        return out
+
+    # ---- device helpers ----
+    def empty(self, *shape, dtype=None):
+        torch = _torch()
+        return torch.empty(shape, dtype=dtype or torch.int32, device="cuda")
+
+    def call(self, name, *args):
+        nat.call(name, self._h, *args)
+
+    def stream(self):
+        return nat.stream_handle()
+
+    def small_to_ntt(self, small: np.ndarray, montgomery=False):
+        """(B, N) signed small ints -> (B, k, N) NTT (device order)."""
+        torch = _torch()
+        s = np.asarray(small, dtype=np.int8).reshape(-1, self.n)
+        d = torch.from_numpy(s).cuda()
+        out = self.empty(s.shape[0], self.k, self.n)
+        self.call("hefv_small_to_rns", d.data_ptr(), out.data_ptr(), s.shape[0], 1,
+                  1 if montgomery else 0, self.stream())
+        return out
+
+    def upload_residues(self, arr: np.ndarray):
+        torch = _torch()
+        return torch.from_numpy(np.ascontiguousarray(np.asarray(arr, dtype=np.int64)
+                                                     .astype(np.int32))).cuda()
+
+    def ntt_q(self, stacks, inverse=False, natural=False):
+        """In-device transform of (B, k, N) stacks under the q primes."""
+        out = _torch().empty_like(stacks)
+        b = stacks.numel() // (self.k * self.n)
+        self.call("hefv_ntt_inv32" if inverse else "hefv_ntt_fwd32", stacks.data_ptr(),
+                  out.data_ptr(), b, self.k, 0, 1 if natural else 0, self.stream())
+        return out
+
+    def elementwise(self, op, a, b, c=None, b_rows=None, c_rows=None):
+        out = _torch().empty_like(a)
+        rows = a.numel() // (self.k * self.n)
+        br = b_rows if b_rows is not None else b.numel() // (self.k * self.n)
+        cr = (c_rows if c_rows is not None else c.numel() // (self.k * self.n)) if c is not None else 1
+        self.call("hefv_elementwise", op, a.data_ptr(), b.data_ptr(), nat.ptr(c),
+                  out.data_ptr(), rows, br, cr, self.stream())
+        return out
+
+    def to_mont(self, a):
+        out = _torch().empty_like(a)
+        self.call("hefv_to_montgomery", a.data_ptr(), out.data_ptr(),
+                  a.numel() // (self.k * self.n), self.stream())
+        return out
+
+    def dev_to_natural(self, stacks_dev_order) -> np.ndarray:
+        """Host copy of device-order NTT stacks in the reference's natural order."""
+        host = stacks_dev_order.cpu().numpy().astype(np.int64)
+        out = np.empty_like(host)
+        out[..., self.brev] = host
+        return out
+
+    def natural_to_dev(self, stacks_natural: np.ndarray) -> np.ndarray:
+        return np.asarray(stacks_natural)[..., self.brev]
+
+
+# ---------------------------------------------------------------------------
+# keys
+# ---------------------------------------------------------------------------
+class SwitchKey:
+    """Key-switch material, device-resident (fv.py:67-72).
+
+    ``body_dev``/``mask_dev``: (k, k, N) [target prime j][digit i], device NTT
+    order, Montgomery form.  ``body``/``mask`` give the reference's layout
+    (list over j of (k, N) natural-order int64) on demand."""
+
+    def __init__(self, ctx: FvContext, body_dev, mask_dev):
+        self._ctx = ctx
+        self.body_dev = body_dev
+        self.mask_dev = mask_dev
+
+    def _host(self, dev):
+        ctx = self._ctx
+        torch = _torch()
+        # undo Montgomery form: x * 2^-32 == mont(x, 1) -- do it on the host exactly
+        host = dev.cpu().numpy().astype(np.int64)
+        out = []
+        for j, p in enumerate(ctx.q_primes):
+            rinv = pow(1 << 32, -1, p)
+            plain = (host[j].astype(object) * rinv % p).astype(np.int64)
+            nat_order = np.empty_like(plain)
+            nat_order[..., ctx.brev] = plain
+            out.append(nat_order)
+        del torch
+        return out
+
+    @property
+    def body(self):
+        return self._host(self.body_dev)
+
+    @property
+    def mask(self):
+        return self._host(self.mask_dev)
+
+
+@dataclass
+class KeySet:
+    """Secret/public/evaluation keys plus the shared context (fv.py:220-228)."""
+
+    context: FvContext
+    secret_small: np.ndarray
+    pk_ntt: object          # (2, k, N) device order, canonical
+    relin: SwitchKey
+    galois: dict
+    s_ntt: object = None    # (k, N) canonical device order
+    _cache: dict = field(default_factory=dict)
+
+    @property
+    def secret(self) -> np.ndarray:
+        return self.context.to_rns(self.secret_small)
+
+    @property
+    def public(self) -> tuple:
+        """(pk0, pk1) coefficient stacks, as the reference stores them."""
+        if "public" not in self._cache:
+            ctx = self.context
+            coeff = ctx.ntt_q(self.pk_ntt.contiguous(), inverse=True)
+            host = coeff.cpu().numpy().astype(np.int64)
+            self._cache["public"] = (host[0], host[1])
+        return self._cache["public"]
+
+
+def _switch_key(ctx: FvContext, s_ntt, target_ntt, rng) -> SwitchKey:
+    """Digit keys switching ``target`` back to ``s`` (fv.py:176-202); the
+    Generator is consumed digit by digit exactly as the reference does."""
+    torch = _torch()
+    k, n = ctx.k, ctx.n
+    body = torch.empty((k, k, n), dtype=torch.int32, device="cuda")
+    mask = torch.empty_like(body)
+    st = ctx.stream()
+    for i in range(k):
+        a = ctx.rand_uniform(rng)
+        e = ctx.rand_error(rng)
+        a_d = torch.from_numpy(a.astype(np.int32)).cuda()
+        e_d = torch.from_numpy(e.astype(np.int8)).cuda()
+        ctx.call("hefv_keygen_digit", a_d.data_ptr(), e_d.data_ptr(), i,
+                 ctx.d_gadget[i].data_ptr(), s_ntt.data_ptr(), target_ntt.data_ptr(),
+                 body.data_ptr(), mask.data_ptr(), st)
+    return SwitchKey(ctx, body, mask)
+
+
+def keygen(fp: FvParams, rotation_offsets=None, rng=None) -> KeySet:
+    """Generate keys (fv.py:231-251) with the same Generator stream."""
+    rng = rng if rng is not None else np.random.default_rng()
+    ctx = FvContext(fp)
+    s = ctx.rand_ternary(rng)
+    a = ctx.rand_uniform(rng)
+    e = ctx.rand_error(rng)
+    s_ntt = ctx.small_to_ntt(s)[0]
+    a_ntt = ctx.ntt_q(ctx.upload_residues(a)[None])[0]
+    e_ntt = ctx.small_to_ntt(e)[0]
+    pk0 = ctx.elementwise(3, a_ntt, s_ntt, e_ntt)  # -(a s + e)
+    pk_ntt = _torch().stack([pk0, a_ntt])
+    s2_ntt = ctx.elementwise(2, s_ntt, s_ntt)
+    relin = _switch_key(ctx, s_ntt, s2_ntt, rng)
+    half = fp.n // 2
+    offsets = {1 << j for j in range((half - 1).bit_length())}
+    if rotation_offsets:
+        offsets |= {off % half for off in rotation_offsets if off % half}
+    galois = {}
+    for off in sorted(offsets):
+        g = galois_element(off, fp.n)
+        tgt = ctx.small_to_ntt(ctx.galois_small(s, g))[0]
+        galois[off] = _switch_key(ctx, s_ntt, tgt, rng)
+    return KeySet(context=ctx, secret_small=s.astype(np.int8), pk_ntt=pk_ntt, relin=relin,
+                  galois=galois, s_ntt=s_ntt)
+
+
+# ---------------------------------------------------------------------------
+# ciphertexts
+# ---------------------------------------------------------------------------
+class FvCiphertext:
+    """RNS ciphertext, resident in HBM as a (parts, k, N) uint32 tensor.
+
+    ``parts`` reads as the reference's list of (k, N) int64 stacks
+    (fv.py:30-42); assigning host parts uploads lazily."""
+
+    __slots__ = ("_dev", "_host", "level_used", "params", "_live")
+
+    def __init__(self, parts, level_used, params, dev=None):
+        self._dev = dev
+        self._host = None if parts is None else [np.asarray(p, dtype=np.int64) for p in parts]
+        self.level_used = level_used
+        self.params = params
+        self._live = True
+
+    @property
+    def parts(self):
+        if self._host is None:
+            host = self._dev.cpu().numpy().astype(np.int64)
+            self._host = [host[i] for i in range(host.shape[0])]
+        return self._host
+
+    @parts.setter
+    def parts(self, value):
+        self._host = [np.asarray(p, dtype=np.int64) for p in value]
+        self._dev = None
+
+    def device(self):
+        if self._dev is None:
+            torch = _torch()
+            stack = np.stack(self._host).astype(np.int32)
+            self._dev = torch.from_numpy(stack).cuda()
+        return self._dev
+
+    @property
+    def nparts(self) -> int:
+        return self._dev.shape[0] if self._dev is not None else len(self._host)
+
+    def __repr__(self):
+        return f"FvCiphertext(parts={self.nparts}, level={self.level_used})"
+
+
+# ---------------------------------------------------------------------------
+# backend
+# ---------------------------------------------------------------------------
+class FvBackend(SlotBackend):
+    """GPU implementation of the slot contract (fv.py:254-432)."""
+
+    def __init__(self, params: BackendParams, keys: KeySet = None, rng=None):
+        if params.slot_count != params.ring_dimension // 2:
+            raise ParamMismatchError("FV backend requires slot_count = n/2")
+        super().__init__(params)
+        self.rng = rng if rng is not None else np.random.default_rng()
+        if keys is None:
+            keys = keygen(FvParams.from_backend(params), rng=self.rng)
+        self.keys = keys
+        self.ctx = keys.context
+        if self.ctx.t != params.plain_modulus or self.ctx.n != params.ring_dimension:
+            raise ParamMismatchError("key set was generated for different parameters")
+        ctx = self.ctx
+        self._s_mont = ctx.to_mont(keys.s_ntt)
+        self._s2_mont = ctx.to_mont(ctx.elementwise(2, keys.s_ntt, keys.s_ntt))
+        self._pk_mont = ctx.to_mont(keys.pk_ntt.contiguous())
+        self._e0_ntt = None
+
+    # ---- batching ----------------------------------------------------------
+    def _slots_dev(self, vecs):
+        torch = _torch()
+        arr = np.asarray(vecs)
+        arr = np.array(arr.tolist(), dtype=np.uint64) if arr.dtype == object else arr.astype(np.uint64)
+        arr = arr.reshape(-1, self.ctx.n // 2)
+        return torch.from_numpy(arr.view(np.int64)).cuda()
+
+    def _encode_dev(self, vecs):
+        """(B, N/2) slot vectors -> (B, N) plaintext polys mod t (device)."""
+        sl = self._slots_dev(vecs)
+        out = self.ctx.empty(sl.shape[0], self.ctx.n, dtype=_torch().int64)
+        self.ctx.call("hefv_encode", sl.data_ptr(), out.data_ptr(), sl.shape[0], self.ctx.stream())
+        return out
+
+    def _decode_dev(self, polys):
+        out = self.ctx.empty(polys.shape[0], self.ctx.n // 2, dtype=_torch().int64)
+        self.ctx.call("hefv_decode", polys.data_ptr(), out.data_ptr(), polys.shape[0],
+                      self.ctx.stream())
+        return out
+
+    def _host_plain(self, dev) -> np.ndarray:
+        arr = dev.cpu().numpy()
+        return arr if self.ctx.t < (1 << 31) else arr.astype(object)
+
+    def encode(self, vec) -> np.ndarray:
+        """Slot vector -> plaintext polynomial mod t (fv.py:280-285)."""
+        t = self.ctx.t
+        v = np.asarray(vec, dtype=object) % t if np.asarray(vec).dtype == object else \
+            np.mod(np.asarray(vec, dtype=np.int64), t)
+        return self._host_plain(self._encode_dev(v)[0])
+
+    def decode(self, poly) -> np.ndarray:
+        t = self.ctx.t
+        p = np.asarray(poly)
+        p = np.array([int(x) % t for x in p], dtype=np.uint64) if p.dtype == object else \
+            np.mod(p.astype(np.int64), t).astype(np.uint64)
+        dev = _torch().from_numpy(p.view(np.int64).reshape(1, -1)).cuda()
+        return self._host_plain(self._decode_dev(dev)[0])
+
+    def _rns_plain(self, polys, mode, to_ntt, montgomery):
+        out = self.ctx.empty(polys.shape[0], self.ctx.k, self.ctx.n)
+        self.ctx.call("hefv_plain_to_rns", polys.data_ptr(), out.data_ptr(), polys.shape[0],
+                      mode, 1 if to_ntt else 0, 1 if montgomery else 0, self.ctx.stream())
+        return out
+
+    def _delta_m_dev(self, vec):
+        return self._rns_plain(self._encode_dev(vec), 0, False, False)
+
+    def _cmult_plain_dev(self, vec):
+        return self._rns_plain(self._encode_dev(vec), 1, True, True)
+
+    # ---- primitives -----------------------------------------------------------
+    def _fresh(self, dev, level):
+        return FvCiphertext(None, level, self.params, dev=dev)
+
+    def _encrypt(self, vec):
+        return self._encrypt_many(np.asarray(vec)[None])[0]
+
+    def _encrypt_many(self, vecs):
+        """Encrypt B slot vectors; the Generator is consumed per ciphertext in
+        the reference's order (u, e1, e2)."""
+        torch = _torch()
+        ctx = self.ctx
+        B = len(vecs)
+        u = np.empty((B, ctx.n), np.int8)
+        e1 = np.empty((B, ctx.n), np.int8)
+        e2 = np.empty((B, ctx.n), np.int8)
+        for b in range(B):
+            u[b] = ctx.rand_ternary(self.rng)
+            e1[b] = ctx.rand_error(self.rng)
+            e2[b] = ctx.rand_error(self.rng)
+        dm = self._delta_m_dev(np.stack([np.asarray(v) for v in vecs]))
+        out = ctx.empty(B, 2, ctx.k, ctx.n)
+        ud, e1d, e2d = (torch.from_numpy(x).cuda() for x in (u, e1, e2))
+        ctx.call("hefv_encrypt", self._pk_mont.data_ptr(), ud.data_ptr(), e1d.data_ptr(),
+                 e2d.data_ptr(), dm.data_ptr(), out.data_ptr(), B, ctx.stream())
+        return [self._fresh(out[b], 0) for b in range(B)]
+
+    def _decrypt_poly_dev(self, devs):
+        ctx = self.ctx
+        torch = _torch()
+        nparts = devs[0].shape[0]
+        cts = torch.stack(devs) if len(devs) > 1 else devs[0][None]
+        B = cts.shape[0]
+        out = ctx.empty(B, ctx.n, dtype=torch.int64)
+        scratch = ctx.empty(B, ctx.k, ctx.n)
+        ctx.call("hefv_decrypt", cts.data_ptr(), nparts, self._s_mont.data_ptr(),
+                 self._s2_mont.data_ptr(), out.data_ptr(), scratch.data_ptr(), B, ctx.stream())
+        return out
+
+    def decrypt_poly(self, ct: FvCiphertext) -> np.ndarray:
+        """Plaintext polynomial mod t (fv.py:337-349)."""
+        return self._host_plain(self._decrypt_poly_dev([ct.device()])[0])
+
+    def _decrypt(self, ct):
+        slots = self._decode_dev(self._decrypt_poly_dev([ct.device()]))[0]
+        return np.asarray(self._host_plain(slots), dtype=self._dtype)
+
+    def decrypt_many(self, cts) -> list:
+        """Batched decryption of several ciphertexts (one launch per stage)."""
+        if not cts:
+            return []
+        for ct in cts:
+            self._check_params(ct)
+        groups = {}
+        for i, ct in enumerate(cts):
+            groups.setdefault(ct.nparts, []).append(i)
+        res = [None] * len(cts)
+        for _, idx in groups.items():
+            slots = self._decode_dev(self._decrypt_poly_dev([cts[i].device() for i in idx]))
+            host = slots.cpu().numpy()
+            for r, i in enumerate(idx):
+                res[i] = np.asarray(host[r] if self.ctx.t < (1 << 31) else host[r].astype(object),
+                                    dtype=self._dtype)
+        return res
+
+    def _add(self, a, b, level):
+        da, db = a.device(), b.device()
+        m = min(da.shape[0], db.shape[0])
+        out = self.ctx.elementwise(0, da[:m].contiguous(), db[:m].contiguous())
+        return self._fresh(out, level)
+
+    def _add_plain(self, a, vec, level):
+        dm = self._delta_m_dev(np.asarray(vec)[None])
+        da = a.device()
+        out = da.clone()
+        out[0] = self.ctx.elementwise(0, da[0].contiguous(), dm[0])
+        return self._fresh(out, level)
+
+    def _cmult(self, a, vec, level):
+        m = self._cmult_plain_dev(np.asarray(vec)[None])
+        da = a.device()
+        out = _torch().empty_like(da)
+        self.ctx.call("hefv_mul_plain", da.data_ptr(), m.data_ptr(), out.data_ptr(), 1,
+                      da.shape[0], 1, self.ctx.stream())
+        return self._fresh(out, level)
+
+    def _mult(self, a, b, level):
+        ctx = self.ctx
+        da = a.device().contiguous()
+        db = da if b is a else b.device().contiguous()
+        out3 = ctx.empty(3, ctx.k, ctx.n)
+        scratch = ctx.empty(7 * ctx.a * ctx.n)
+        ctx.call("hefv_mult_tensor", da.data_ptr(), db.data_ptr(), out3.data_ptr(),
+                 scratch.data_ptr(), ctx.stream())
+        return self._relinearize(out3, level)
+
+    def _relinearize(self, out3, level):
+        ctx = self.ctx
+        out = ctx.empty(2, ctx.k, ctx.n)
+        key = self.keys.relin
+        stack = ctx.k * ctx.n
+        ctx.call("hefv_keyswitch", key.body_dev.data_ptr(), key.mask_dev.data_ptr(),
+                 out3[2].data_ptr(), 0, out[0].data_ptr(), out[1].data_ptr(), 0, None,
+                 out3[0].data_ptr(), out3[1].data_ptr(), 0, None, None, 0, 1, ctx.stream())
+        del stack
+        return self._fresh(out, level)
+
+    def rotation_hops(self, offset: int) -> list:
+        """Key-switch hops of a rotation (fv.py:422-425)."""
+        if offset == 0:
+            return []
+        if offset in self.keys.galois:
+            return [offset]
+        return [1 << j for j in range(offset.bit_length()) if offset >> j & 1]
+
+    def _hop(self, dev, off):
+        ctx = self.ctx
+        g = galois_element(off, ctx.n)
+        scratch = ctx.empty(2, ctx.k, ctx.n)
+        ctx.call("hefv_automorph", dev.data_ptr(), 0, None, scratch.data_ptr(), 2, g, 1,
+                 ctx.stream())
+        out = ctx.empty(2, ctx.k, ctx.n)
+        key = self.keys.galois[off]
+        ctx.call("hefv_keyswitch", key.body_dev.data_ptr(), key.mask_dev.data_ptr(),
+                 scratch[1].data_ptr(), 0, out[0].data_ptr(), out[1].data_ptr(), 0, None,
+                 scratch[0].data_ptr(), None, 0, None, None, 0, 1, ctx.stream())
+        return out
+
+    def _rotate(self, a, offset, level):
+        dev = a.device()
+        if offset == 0:
+            return self._fresh(dev.clone(), level)
+        dev = dev[:2].contiguous()
+        for off in self.rotation_hops(offset):
+            dev = self._hop(dev, off)
+        return self._fresh(dev, level)
+
+    # ---- helpers for the layer planner ---------------------------------------------
+    def e0_plain_ntt(self):
+        """Montgomery NTT of centred(encode(e0)), cached (inference.py:287, 327)."""
+        if self._e0_ntt is None:
+            self._e0_ntt = self._cmult_plain_dev(self.one_hot(0)[None])
+        return self._e0_ntt
+
+
+# ---------------------------------------------------------------------------
+# op-sequence runner and conformance check (fv.py:435-479)
+# ---------------------------------------------------------------------------
+def run_sequence(backend: SlotBackend, ops) -> list:
+    """Execute a declarative op list; returns the value stack."""
+    stack = []
+    for op in ops:
+        kind = op[0]
+        if kind == "enc":
+            stack.append(backend.encrypt(op[1]))
+        elif kind == "add":
+            stack.append(backend.add(stack[op[1]], stack[op[2]]))
+        elif kind == "mult":
+            stack.append(backend.mult(stack[op[1]], stack[op[2]]))
+        elif kind == "cmult":
+            stack.append(backend.cmult(stack[op[1]], op[2]))
+        elif kind == "add_plain":
+            stack.append(backend.add_plain(stack[op[1]], op[2]))
+        elif kind == "rotate":
+            stack.append(backend.rotate(stack[op[1]], op[2]))
+        elif kind == "psum":
+            stack.append(backend.partial_sum(stack[op[1]], op[2]))
+        elif kind == "asum":
+            stack.append(backend.all_sum(stack[op[1]], op[2]))
+        else:
+            raise ValueError(f"unknown op {kind!r}")
+    return stack
+
+
+def fv_conformance(fv_backend, sim_backend, ops) -> bool:
+    """Run ``ops`` on both backends; False on the first decryption mismatch."""
+    fv_stack = run_sequence(fv_backend, ops)
+    sim_stack = run_sequence(sim_backend, ops)
+    for f, s in zip(fv_stack, sim_stack):
+        got = np.asarray(fv_backend.decrypt(f), dtype=np.int64)
+        want = np.asarray(sim_backend.decrypt(s), dtype=np.int64)
+        if not np.array_equal(got, want):
+            return False
+    return True

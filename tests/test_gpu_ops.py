@@ -1,0 +1,165 @@
+"""GPU parity: every FV primitive bit-identical to the CPU oracle.
+
+The oracle (oracle/fv_oracle.py) is pinned to the reference by
+tests/test_oracle.py; here the CUDA path (through the C-ABI) must produce
+the same ciphertext limbs under the same seeded keys and randomness.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import fv_oracle as O
+from paper_1901_10074_b200.params import BackendParams, profile
+
+pytestmark = pytest.mark.gpu
+
+
+def _digest(parts):
+    return O.limb_digest(parts)
+
+
+# ---------------------------------------------------------------- NTT
+@pytest.mark.parametrize("n,bits", [(16, 30), (64, 30), (1024, 30), (4096, 30), (16384, 30),
+                                    (32768, 30), (64, 20), (4096, 50), (16384, 60),
+                                    (32768, 55), (65536, 60)])
+def test_ntt_matches_oracle(n, bits, rng):
+    from paper_1901_10074_b200.ntt import NttPrime
+
+    p = O.ntt_primes(1, bits, 2 * n)[0]
+    ref = O.OracleNtt(p, n)
+    gpu = NttPrime(p, n)
+    assert gpu.psi == ref.psi
+    a = np.array([int(rng.integers(0, p)) for _ in range(3 * n)], dtype=object).reshape(3, n)
+    want = ref.fwd(a)
+    got = gpu.fwd(a)
+    assert np.array_equal(np.asarray(got, dtype=object), np.asarray(want, dtype=object))
+    back = gpu.inv(got)
+    assert np.array_equal(np.asarray(back, dtype=object), np.asarray(a % p, dtype=object))
+
+
+def test_ntt_negacyclic_against_schoolbook(rng):
+    from paper_1901_10074_b200.ntt import NttPrime
+
+    n = 64
+    p = O.ntt_primes(1, 30, 2 * n)[0]
+    tr = NttPrime(p, n)
+    a = rng.integers(0, p, n)
+    b = rng.integers(0, p, n)
+    want = O.schoolbook(a, b, n, p).astype(np.int64)
+    assert np.array_equal(tr.negacyclic_mul(a, b), want)
+
+
+# ---------------------------------------------------------------- FV desk
+@pytest.fixture(scope="module")
+def desk_pair():
+    from paper_1901_10074_b200.fv import FvBackend
+
+    p = profile("desk")
+    gpu = FvBackend(p, rng=np.random.default_rng(77))
+    orc = O.OracleFvBackend(p, rng=np.random.default_rng(77))
+    return gpu, orc
+
+
+def test_keys_match_oracle(desk_pair):
+    gpu, orc = desk_pair
+    assert np.array_equal(gpu.keys.secret, orc.keys.secret)
+    for j in (0, 3, 5):
+        assert np.array_equal(gpu.keys.relin.body[j], orc.keys.relin.body[j])
+        assert np.array_equal(gpu.keys.relin.mask[j], orc.keys.relin.mask[j])
+    assert sorted(gpu.keys.galois) == sorted(orc.keys.galois)
+    for off in (1, 64, 1024):
+        assert np.array_equal(gpu.keys.galois[off].body[2], orc.keys.galois[off].body[2])
+    assert np.array_equal(gpu.keys.public[0], orc.keys.public[0])
+    assert np.array_equal(gpu.keys.public[1], orc.keys.public[1])
+
+
+def test_encode_decode_match(desk_pair, rng):
+    gpu, orc = desk_pair
+    t = gpu.params.plain_modulus
+    v = rng.integers(0, t, gpu.params.slot_count)
+    assert np.array_equal(gpu.encode(v), orc.encode(v))
+    assert np.array_equal(gpu.decode(gpu.encode(v)), v % t)
+
+
+def test_ops_bit_identical(desk_pair, rng):
+    gpu, orc = desk_pair
+    t = gpu.params.plain_modulus
+    v = rng.integers(0, t, gpu.params.slot_count)
+    w = rng.integers(0, t, gpu.params.slot_count)
+    ga, oa = gpu.encrypt(v), orc.encrypt(v)
+    assert _digest(ga.parts) == _digest(oa.parts)
+    gb, ob = gpu.encrypt(w), orc.encrypt(w)
+    cases = {
+        "add": (gpu.add(ga, gb), orc.add(oa, ob)),
+        "add_plain": (gpu.add_plain(ga, w), orc.add_plain(oa, w)),
+        "cmult": (gpu.cmult(ga, w), orc.cmult(oa, w)),
+        "rotate1": (gpu.rotate(ga, 1), orc.rotate(oa, 1)),
+        "rotate129": (gpu.rotate(ga, 129), orc.rotate(oa, 129)),
+        "rotate-17": (gpu.rotate(ga, -17), orc.rotate(oa, -17)),
+        "mult": (gpu.mult(ga, gb), orc.mult(oa, ob)),
+        "square": (gpu.mult(ga, ga), orc.mult(oa, oa)),
+    }
+    for name, (g, o) in cases.items():
+        assert g.level_used == o.level_used, name
+        assert _digest(g.parts) == _digest(o.parts), name
+        assert np.array_equal(gpu.decrypt(g), orc.decrypt(o)), name
+
+
+def test_decrypt_poly_and_three_parts(desk_pair, rng):
+    gpu, orc = desk_pair
+    t = gpu.params.plain_modulus
+    v = rng.integers(0, t, gpu.params.slot_count)
+    ga, oa = gpu.encrypt(v), orc.encrypt(v)
+    assert np.array_equal(np.asarray(gpu.decrypt_poly(ga), dtype=np.int64),
+                          np.asarray(orc.decrypt_poly(oa), dtype=np.int64))
+    # unrelinearised 3-part ciphertext decrypts with s^2
+    t3 = orc.tensor(oa, oa)
+    from paper_1901_10074_b200.fv import FvCiphertext
+
+    g3 = FvCiphertext(t3, 1, gpu.params)
+    o3 = O.OracleCiphertext(t3, 1, orc.params)
+    assert np.array_equal(np.asarray(gpu.decrypt_poly(g3), dtype=np.int64),
+                          np.asarray(orc.decrypt_poly(o3), dtype=np.int64))
+
+
+def test_folds_and_levels(desk_pair, rng):
+    gpu, orc = desk_pair
+    t = gpu.params.plain_modulus
+    v = rng.integers(0, t, gpu.params.slot_count)
+    ga, oa = gpu.encrypt(v), orc.encrypt(v)
+    g = gpu.all_sum(gpu.cmult(ga, [1] * 100), 100)
+    o = orc.all_sum(orc.cmult(oa, [1] * 100), 100)
+    assert _digest(g.parts) == _digest(o.parts)
+    g = gpu.partial_sum(ga, 8)
+    o = orc.partial_sum(oa, 8)
+    assert _digest(g.parts) == _digest(o.parts)
+
+
+def test_host_parts_roundtrip(desk_pair, rng):
+    from paper_1901_10074_b200.fv import FvCiphertext
+
+    gpu, orc = desk_pair
+    t = gpu.params.plain_modulus
+    v = rng.integers(0, t, gpu.params.slot_count)
+    oa = orc.encrypt(v)
+    ga = FvCiphertext([p.copy() for p in oa.parts], 0, gpu.params)
+    assert np.array_equal(gpu.decrypt(ga), v % t)
+    g = gpu.rotate(ga, 5)
+    o = orc.rotate(oa, 5)
+    assert _digest(g.parts) == _digest(o.parts)
+
+
+# ---------------------------------------------------------------- small custom params
+def test_tiny_params_all_ops(rng):
+    from paper_1901_10074_b200.fv import FvBackend
+
+    p = BackendParams(ring_dimension=64, coeff_modulus_bits=120, plain_modulus=257,
+                      slot_count=32, depth_budget=4)
+    gpu = FvBackend(p, rng=np.random.default_rng(5))
+    orc = O.OracleFvBackend(p, rng=np.random.default_rng(5))
+    v = rng.integers(0, 257, 32)
+    ga, oa = gpu.encrypt(v), orc.encrypt(v)
+    assert _digest(ga.parts) == _digest(oa.parts)
+    for g, o in [(gpu.mult(ga, ga), orc.mult(oa, oa)), (gpu.rotate(ga, 7), orc.rotate(oa, 7)),
+                 (gpu.cmult(ga, v), orc.cmult(oa, v))]:
+        assert _digest(g.parts) == _digest(o.parts)
