@@ -416,6 +416,9 @@ class FvCiphertext:
 class FvBackend(SlotBackend):
     """GPU implementation of the slot contract (fv.py:254-432)."""
 
+    # layer_eval dispatches to the batched planner for this backend
+    batched_layers = True
+
     def __init__(self, params: BackendParams, keys: KeySet = None, rng=None):
         if params.slot_count != params.ring_dimension // 2:
             raise ParamMismatchError("FV backend requires slot_count = n/2")
@@ -491,6 +494,17 @@ class FvBackend(SlotBackend):
 
     def _encrypt(self, vec):
         return self._encrypt_many(np.asarray(vec)[None])[0]
+
+    def encrypt_many(self, values_list) -> list:
+        """``[encrypt(v) for v in values_list]`` with one launch per stage; the
+        Generator and the ledger see exactly the per-call sequence."""
+        plains = [self.as_plain(v) for v in values_list]
+        if not plains:
+            return []
+        cts = self._encrypt_many(plains)
+        for _ in cts:
+            self._c.bump("encrypt", level=0)
+        return cts
 
     def _encrypt_many(self, vecs):
         """Encrypt B slot vectors; the Generator is consumed per ciphertext in

@@ -1,0 +1,228 @@
+"""Generate the golden fixtures by running the REFERENCE itself.
+
+Run in the build container (where /root/reference exists):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [--retina]
+
+Writes tests/golden/{ntt,primes,fv_desk,fv_tiny,config1}.json (and
+retina.json with --retina, ~4 min).  Fixtures hold seeds, small inputs and
+sha256 digests of the reference's int64 limbs (oracle.fv_oracle.limb_digest
+layout), plus full vectors where they are small.  The reference is imported
+only here; tests read the JSON.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, "/root/reference/pkg/src")
+HERE = Path(__file__).resolve().parent
+
+from hepack import engine as R_engine  # noqa: E402
+from hepack import fv as R_fv  # noqa: E402
+from hepack import inference as R_inf  # noqa: E402
+from hepack import ntt as R_ntt  # noqa: E402
+from hepack.params import BackendParams, profile  # noqa: E402
+
+
+def digest(parts) -> str:
+    h = hashlib.sha256()
+    for p in parts:
+        h.update(np.ascontiguousarray(np.asarray(p, dtype=np.int64)).astype("<i8").tobytes())
+    return h.hexdigest()
+
+
+def vec_digest(v) -> str:
+    return digest([np.asarray([int(x) for x in v], dtype=np.int64)])
+
+
+def key_digest(sk) -> str:
+    return digest(list(sk.body) + list(sk.mask))
+
+
+def dump(name, obj):
+    (HERE / name).write_text(json.dumps(obj, indent=1, sort_keys=True))
+    print("wrote", name)
+
+
+def gen_ntt():
+    cases = []
+    for n, bits in [(8, 30), (64, 30), (256, 30), (16, 20), (4096, 30), (16384, 30),
+                    (32768, 30), (4096, 50), (16384, 60), (32768, 55), (65536, 60)]:
+        p = R_ntt.find_ntt_primes(1, bits, 2 * n)[0]
+        tr = R_ntt.NttPrime(p, n)
+        rng = np.random.default_rng(n * 1000 + bits)
+        a = np.array([int(rng.integers(0, p)) for _ in range(n)], dtype=object)
+        fa = tr.fwd(a)
+        case = {"n": n, "bits": bits, "p": p, "psi": tr.psi, "seed": n * 1000 + bits,
+                "in_digest": vec_digest(a), "fwd_digest": vec_digest(fa),
+                "fwd_head": [int(x) for x in fa[:4]],
+                "inv_roundtrip": bool(all(int(x) == int(y) for x, y in zip(tr.inv(fa), a)))}
+        if n <= 256:
+            case["in"] = [int(x) for x in a]
+            case["fwd"] = [int(x) for x in fa]
+        cases.append(case)
+    dump("ntt.json", {"cases": cases})
+
+
+def gen_primes():
+    out = {}
+    for name in ("desk", "mnist", "retina"):
+        fp = R_fv.FvParams.from_backend(profile(name))
+        ctx = R_fv._FvContext(fp)
+        out[name] = {"q": fp.q_primes, "aux": ctx.aux_primes, "t_psi": ctx.t_ntt.psi,
+                     "q_psi": [tr.psi for tr in ctx.q_ntt],
+                     "slot_to_ev_digest": vec_digest(ctx.slot_to_ev),
+                     "gadget_digest": vec_digest([g % (1 << 61) for g in ctx.gadget])}
+    p720 = profile("retina").replace(coeff_modulus_bits=720)
+    fp = R_fv.FvParams.from_backend(p720)
+    ctx = R_fv._FvContext(fp)
+    out["retina-720"] = {"q": fp.q_primes, "aux": ctx.aux_primes}
+    dump("primes.json", out)
+
+
+def op_suite(be, rng, slots, t):
+    """The op sequence replayed by the GPU/oracle tests (same order of draws)."""
+    v = rng.integers(0, t, slots)
+    w = rng.integers(0, t, slots)
+    a = be.encrypt(v)
+    b = be.encrypt(w)
+    res = {"v": vec_digest(v), "w": vec_digest(w), "enc_a": digest(a.parts),
+           "enc_b": digest(b.parts)}
+    ops = [
+        ("add", lambda: be.add(a, b)),
+        ("add_plain", lambda: be.add_plain(a, w)),
+        ("cmult", lambda: be.cmult(a, w)),
+        ("rotate1", lambda: be.rotate(a, 1)),
+        ("rotate129", lambda: be.rotate(a, 129 % slots)),
+        ("rotate-17", lambda: be.rotate(a, -17)),
+        ("mult", lambda: be.mult(a, b)),
+        ("square", lambda: be.mult(a, a)),
+        ("allsum", lambda: be.all_sum(be.cmult(a, [1] * min(100, slots)), min(100, slots))),
+        ("psum8", lambda: be.partial_sum(a, 8)),
+    ]
+    for name, fn in ops:
+        ct = fn()
+        res[name] = digest(ct.parts)
+        res[name + "_dec"] = vec_digest(be.decrypt(ct))
+        res[name + "_level"] = ct.level_used
+    res["decpoly_a"] = vec_digest(be.decrypt_poly(a))
+    res["cost"] = be.cost_report().as_dict()
+    return res
+
+
+def gen_fv_desk():
+    p = profile("desk")
+    be = R_fv.FvBackend(p, rng=np.random.default_rng(77))
+    k = be.keys
+    out = {"seed": 77, "data_seed": 5,
+           "secret": digest([k.secret]), "pk": digest(list(k.public)),
+           "relin": key_digest(k.relin),
+           "galois": {str(off): key_digest(sk) for off, sk in k.galois.items()}}
+    out["ops"] = op_suite(be, np.random.default_rng(5), p.slot_count, p.plain_modulus)
+    dump("fv_desk.json", out)
+
+
+def gen_fv_tiny():
+    p = BackendParams(ring_dimension=64, coeff_modulus_bits=120, plain_modulus=257, slot_count=32,
+                      depth_budget=4)
+    be = R_fv.FvBackend(p, rng=np.random.default_rng(5))
+    rng = np.random.default_rng(9)
+    v = rng.integers(0, 257, 32)
+    a = be.encrypt(v)
+    out = {"params": {"ring_dimension": 64, "coeff_modulus_bits": 120, "plain_modulus": 257,
+                      "slot_count": 32, "depth_budget": 4},
+           "key_seed": 5, "data_seed": 9,
+           "enc": [p_.tolist() for p_ in a.parts],
+           "square": [p_.tolist() for p_ in be.mult(a, a).parts],
+           "rotate7": [p_.tolist() for p_ in be.rotate(a, 7).parts],
+           "cmult": [p_.tolist() for p_ in be.cmult(a, v).parts]}
+    dump("fv_tiny.json", out)
+
+
+def net_for(cfg):
+    rng = np.random.default_rng(cfg)
+    if cfg == 1:
+        img = rng.integers(0, 256, (1, 16, 16), dtype=np.int64)
+        conv = R_inf.ConvSpec(2, (3, 3), (2, 2), (1, 16, 16), rng.integers(-4, 5, (2, 1, 3, 3)),
+                              np.zeros(2, np.int64))
+        fc = R_inf.FcSpec(2, rng.integers(-4, 5, (2, conv.out_len)), np.zeros(2, np.int64))
+        return img, R_inf.NetworkSpec([conv, R_inf.SquareSpec(), fc], (1, 16, 16))
+    img = rng.integers(0, 256, (1, 96, 96), dtype=np.int64)
+    conv = R_inf.ConvSpec(5, (5, 5), (2, 2), (1, 96, 96), rng.integers(-8, 9, (5, 1, 5, 5)),
+                          np.zeros(5, np.int64))
+    fc = R_inf.FcSpec(2, rng.integers(-8, 9, (2, conv.out_len)), np.zeros(2, np.int64))
+    return img, R_inf.NetworkSpec([conv, R_inf.SquareSpec(), fc], (1, 96, 96))
+
+
+def gen_config1():
+    img, net = net_for(1)
+    be = R_fv.FvBackend(profile("desk"), rng=np.random.default_rng(1234))
+    t0 = time.time()
+    pv = R_inf.pack_image(be, img)
+    enc = [digest(ct.parts) for ct in pv.cts]
+    layers = []
+    cur = pv
+    for layer in net.layers:
+        if isinstance(layer, R_inf.SquareSpec):
+            nxt = R_inf.square_activation(be, cur)
+        else:
+            rows = (R_inf.compile_conv(layer, cur.slots_used) if isinstance(layer, R_inf.ConvSpec)
+                    else R_inf.compile_fc(layer, cur.slots_used))
+            nxt = R_inf.layer_eval(be, rows, cur)
+        if cur is not pv:
+            be.release(*cur.cts)
+        cur = nxt
+        layers.append([digest(ct.parts) for ct in cur.cts])
+    logits = R_inf.decrypt_logits(be, cur)
+    out = {"key_seed": 1234, "data_seed": 1, "enc": enc, "layers": layers,
+           "logits": [int(x) for x in logits], "cost": be.cost_report().as_dict(),
+           "seconds": time.time() - t0}
+    dump("config1.json", out)
+
+
+def gen_retina():
+    p = profile("retina")
+    t0 = time.time()
+    be = R_fv.FvBackend(p, rng=np.random.default_rng(1234))
+    tk = time.time() - t0
+    img, net = net_for(2)
+    k = be.keys
+    pv = R_inf.pack_image(be, img)
+    out = {"key_seed": 1234, "keygen_seconds": tk, "relin": key_digest(k.relin),
+           "galois1": key_digest(k.galois[1]), "galois4096": key_digest(k.galois[4096]),
+           "pk": digest(list(k.public)), "enc": [digest(ct.parts) for ct in pv.cts]}
+    a = pv.cts[0]
+    out["rotate1"] = digest(be.rotate(a, 1).parts)
+    sq = be.mult(a, a)
+    out["square"] = digest(sq.parts)
+    out["square_dec_ok"] = bool(np.array_equal(
+        np.asarray(be.decrypt(sq), dtype=object),
+        np.asarray(be.decrypt(a), dtype=object) ** 2 % p.plain_modulus))
+    # a subset of config-2 conv rows (all in output ciphertext 0)
+    rows = R_inf.compile_conv(net.layers[0], pv.slots_used)
+    pick = [0, 1, 47, 2500, 8191]
+    t1 = time.time()
+    res = R_inf.layer_eval(be, [rows[i] for i in pick], pv)
+    out["rows_pick"] = pick
+    out["rows_out"] = [digest(ct.parts) for ct in res.cts]
+    out["rows_cost"] = be.cost_report().as_dict()
+    out["rows_seconds"] = time.time() - t1
+    dump("retina.json", out)
+
+
+if __name__ == "__main__":
+    gen_ntt()
+    gen_primes()
+    gen_fv_tiny()
+    gen_fv_desk()
+    gen_config1()
+    if "--retina" in sys.argv:
+        gen_retina()
+    del R_engine

@@ -1,0 +1,126 @@
+"""GPU parity of the batched layer planner and of whole encrypted inferences.
+
+* config 1 (desk toy net) end to end against the reference's own run
+  (tests/golden/config1.json: per-layer limb digests, logits, CostReport);
+* a subset of config-2 conv rows at the retina profile against the
+  reference (tests/golden/retina.json);
+* the planner against the serial per-row schedule on the same GPU backend
+  for layouts the configs do not reach (biases, zero rows, several output
+  ciphertexts, skip_zero_segments=False, partial slot use).
+"""
+
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle.fv_oracle import limb_digest
+from paper_1901_10074_b200 import inference as I
+from paper_1901_10074_b200.configs import config_network, config_params
+
+pytestmark = pytest.mark.gpu
+GOLD = Path(__file__).resolve().parent / "golden"
+
+
+def _gold(name):
+    return json.loads((GOLD / name).read_text())
+
+
+def test_config1_end_to_end_matches_reference():
+    from paper_1901_10074_b200.fv import FvBackend
+
+    g = _gold("config1.json")
+    img, net = config_network(1)
+    be = FvBackend(config_params(1), rng=np.random.default_rng(g["key_seed"]))
+    pv = I.pack_image(be, img)
+    assert [limb_digest(ct.parts) for ct in pv.cts] == g["enc"]
+    cur = pv
+    for li, layer in enumerate(net.layers):
+        if isinstance(layer, I.SquareSpec):
+            nxt = I.square_activation(be, cur)
+        else:
+            rows = (I.compile_conv(layer, cur.slots_used) if isinstance(layer, I.ConvSpec)
+                    else I.compile_fc(layer, cur.slots_used))
+            nxt = I.layer_eval(be, rows, cur)
+        if cur is not pv:
+            be.release(*cur.cts)
+        cur = nxt
+        assert [limb_digest(ct.parts) for ct in cur.cts] == g["layers"][li], f"layer {li}"
+    logits = I.decrypt_logits(be, cur)
+    assert [int(v) for v in logits] == g["logits"]
+    assert be.cost_report().as_dict() == g["cost"]
+
+
+def test_config1_infer_api():
+    from paper_1901_10074_b200.fv import FvBackend
+
+    g = _gold("config1.json")
+    img, net = config_network(1)
+    be = FvBackend(config_params(1), rng=np.random.default_rng(g["key_seed"]))
+    out = I.infer(be, net, I.pack_image(be, img))
+    assert [limb_digest(ct.parts) for ct in out.cts] == g["layers"][-1]
+    assert [int(v) for v in I.decrypt_logits(be, out)] == g["logits"]
+
+
+@pytest.mark.slow
+def test_retina_rows_subset_matches_reference():
+    from paper_1901_10074_b200.fv import FvBackend
+
+    g = _gold("retina.json")
+    img, net = config_network(2)
+    be = FvBackend(config_params(2), rng=np.random.default_rng(g["key_seed"]))
+    pv = I.pack_image(be, img)
+    assert [limb_digest(ct.parts) for ct in pv.cts] == g["enc"]
+    # key material bit-identical to the reference's keygen
+    from oracle.fv_oracle import limb_digest as ld
+
+    k = be.keys
+    assert ld(list(k.relin.body) + list(k.relin.mask)) == g["relin"]
+    a = pv.cts[0]
+    assert limb_digest(be.rotate(a, 1).parts) == g["rotate1"]
+    assert limb_digest(be.mult(a, a).parts) == g["square"]
+    rows = I.compile_conv(net.layers[0], pv.slots_used)
+    res = I.layer_eval(be, [rows[i] for i in g["rows_pick"]], pv)
+    assert [limb_digest(ct.parts) for ct in res.cts] == g["rows_out"]
+    assert be.cost_report().as_dict() == g["rows_cost"]
+
+
+def _random_rows(rng, length, s, count, bias=True, zero_rows=True):
+    rows = []
+    for i in range(count):
+        nnz = int(rng.integers(0, 12)) if zero_rows else int(rng.integers(1, 12))
+        pos = np.sort(rng.choice(length, size=nnz, replace=False)).astype(np.int64)
+        vals = rng.integers(-9, 10, nnz)
+        vals[vals == 0] = 3
+        b = int(rng.integers(-5, 6)) if bias and i % 3 == 0 else 0
+        rows.append(I.WeightRow(out_index=i, length=length, slots_used=s, positions=pos,
+                                values=vals.astype(np.int64), bias=b))
+    return rows
+
+
+@pytest.mark.parametrize("s,skip", [(2048, True), (2048, False), (512, True), (100, True)])
+def test_planner_equals_serial(s, skip):
+    from paper_1901_10074_b200.fv import FvBackend
+
+    params = config_params(1)
+    rng = np.random.default_rng(s + skip)
+    length = 3 * s - 17
+    rows = _random_rows(rng, length, s, 40 if s >= 512 else 250)
+    data = rng.integers(0, 50, length)
+
+    results = []
+    for planned in (True, False):
+        be = FvBackend(params, rng=np.random.default_rng(42))
+        x = I.pack_image(be, data.reshape(1, 1, -1), slots_used=s)
+        if planned:
+            out = I.layer_eval(be, rows, x, skip_zero_segments=skip)
+        else:
+            out = I._serial_layer_eval(be, rows, x, skip, 1)
+        results.append(([limb_digest(ct.parts) for ct in out.cts],
+                        [ct.level_used for ct in out.cts], be.cost_report().as_dict(),
+                        I.decrypt_logits(be, out)))
+    assert results[0][0] == results[1][0]
+    assert results[0][1] == results[1][1]
+    assert results[0][2] == results[1][2]
+    assert np.array_equal(results[0][3], results[1][3])
