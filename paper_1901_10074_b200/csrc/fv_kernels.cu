@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(Geo<LOGN, 4>::NT)
   uint64_t x[G_::E];
 #pragma unroll
   for (int e = 0; e < G_::E; ++e) {
-    const int s = dev_to_slot[tid * G_::E + e];
+    const int s = dev_to_slot[row_index<LOGN, 4>(tid, e)];
     x[e] = s >= 0 ? reduce_any(src[s], inf) : 0ull;
   }
   cta_inv<LOGN, 4, Mod64>(md, x, sm, itw_all + (size_t)t_index * G_::N, inf.ninv, inf.wn);
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(Geo<LOGN, 4>::NT)
   __syncthreads();
   uint64_t x[G_::E];
 #pragma unroll
-  for (int e = 0; e < G_::E; ++e) x[e] = sm[spad(tid * G_::E + e)];
+  for (int e = 0; e < G_::E; ++e) x[e] = sm[spad(row_index<LOGN, 4>(tid, e))];
   __syncthreads();
   cta_inv<LOGN, 4, Mod64>(md, x, sm, itw_all + (size_t)t_index * G_::N, inf.ninv, inf.wn);
   uint64_t* dst = poly + b * G_::N;
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(Geo<LOGN, 4>::NT)
   for (int e = 0; e < G_::E; ++e) x[e] = reduce_any(src[tid + e * G_::NT], inf);
   cta_fwd<LOGN, 4, Mod64>(md, x, sm, tw_all + (size_t)t_index * G_::N);
 #pragma unroll
-  for (int e = 0; e < G_::E; ++e) sm[spad(tid * G_::E + e)] = md.canon4(x[e]);
+  for (int e = 0; e < G_::E; ++e) sm[spad(row_index<LOGN, 4>(tid, e))] = md.canon4(x[e]);
   __syncthreads();
   uint64_t* dst = slots + b * (G_::N / 2);
   for (int s = tid; s < G_::N / 2; s += G_::NT) dst[s] = sm[spad(slot_to_dev[s])];
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(Geo<LOGN, Loge32<LOGN>::v>::NT)
     for (int e = 0; e < G_::E; ++e) {
       uint32_t v = md.canon4(x[e]);
       if (montgomery) v = mont_canon(v, inf);
-      dst[tid * G_::E + e] = v;
+      dst[row_index<LOGN, LE>(tid, e)] = v;
     }
   } else {
 #pragma unroll
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(Geo<LOGN, Loge32<LOGN>::v>::NT)
     for (int e = 0; e < G_::E; ++e) {
       uint32_t v = md.canon4(x[e]);
       if (montgomery) v = mont_canon(v, inf);
-      dst[tid * G_::E + e] = v;
+      dst[row_index<LOGN, LE>(tid, e)] = v;
     }
   } else {
 #pragma unroll
@@ -398,9 +398,9 @@ __global__ void __launch_bounds__(Geo<LOGN, Loge32<LOGN>::v>::NT)
   for (int e = 0; e < G_::E; ++e) xu[e] = small_to_mod(u[b * N + tid + e * G_::NT], inf.p);
   cta_fwd<LOGN, LE, Mod32>(md, xu, sm, tw_all + (size_t)j * N);
   for (int part = 0; part < 2; ++part) {
-    const uint32_t* pk = pk_ntt + ((size_t)part * k + j) * N + tid * G_::E;
+    const uint32_t* pk = pk_ntt + ((size_t)part * k + j) * N;
 #pragma unroll
-    for (int e = 0; e < G_::E; ++e) y[e] = mont_mul_lazy(xu[e], pk[e], inf.p, inf.pinv_neg);
+    for (int e = 0; e < G_::E; ++e) y[e] = mont_mul_lazy(xu[e], pk[row_index<LOGN, LE>(tid, e)], inf.p, inf.pinv_neg);
     cta_inv<LOGN, LE, Mod32>(md, y, sm, itw_all + (size_t)j * N, inf.ninv, inf.wn);
     const int8_t* er = (part == 0 ? e1 : e2) + b * N;
     uint32_t* dst = out + ((b * 2 + part) * k + j) * N;
@@ -458,10 +458,10 @@ __global__ void __launch_bounds__(Geo<LOGN, Loge32<LOGN>::v>::NT)
 #pragma unroll
     for (int e = 0; e < G_::E; ++e) x[e] = src[tid + e * G_::NT];
     cta_fwd<LOGN, LE, Mod32>(md, x, sm, tw_all + (size_t)j * N);
-    const uint32_t* sk = (m == 1 ? s_ntt : s2_ntt) + (size_t)j * N + tid * G_::E;
+    const uint32_t* sk = (m == 1 ? s_ntt : s2_ntt) + (size_t)j * N;
 #pragma unroll
     for (int e = 0; e < G_::E; ++e)
-      acc[e] = md.sub2p(acc[e] + mont_mul_lazy(x[e], sk[e], inf.p, inf.pinv_neg));
+      acc[e] = md.sub2p(acc[e] + mont_mul_lazy(x[e], sk[row_index<LOGN, LE>(tid, e)], inf.p, inf.pinv_neg));
     __syncthreads();
   }
   cta_inv<LOGN, LE, Mod32>(md, acc, sm, itw_all + (size_t)j * N, inf.ninv, inf.wn);
@@ -513,9 +513,9 @@ __global__ void __launch_bounds__(Geo<LOGN, Loge32<LOGN>::v>::NT)
 #pragma unroll
   for (int e = 0; e < G_::E; ++e) x[e] = ct[off + tid + e * G_::NT];
   cta_fwd<LOGN, LE, Mod32>(md, x, sm, tw_all + (size_t)j * N);
-  const uint32_t* mm = m_ntt + ((m_broadcast ? 0 : b) * k + j) * N + tid * G_::E;
+  const uint32_t* mm = m_ntt + ((m_broadcast ? 0 : b) * k + j) * N;
 #pragma unroll
-  for (int e = 0; e < G_::E; ++e) x[e] = mont_mul_lazy(x[e], mm[e], inf.p, inf.pinv_neg);
+  for (int e = 0; e < G_::E; ++e) x[e] = mont_mul_lazy(x[e], mm[row_index<LOGN, LE>(tid, e)], inf.p, inf.pinv_neg);
   __syncthreads();
   cta_inv<LOGN, LE, Mod32>(md, x, sm, itw_all + (size_t)j * N, inf.ninv, inf.wn);
 #pragma unroll
@@ -560,11 +560,11 @@ __global__ void __launch_bounds__(Geo<LOGN, Loge32<LOGN>::v>::NT)
   const int lo = row_ptr[r], hi = row_ptr[r + 1];
   for (int p = lo; p < hi; ++p) {
     const int seg = plain_seg[p];
-    const uint32_t* xs = x_ntt + (((size_t)seg * 2 + part) * k + j) * N + tid * G_::E;
-    const uint32_t* ms = m_ntt + ((size_t)p * k + j) * N + tid * G_::E;
+    const uint32_t* xs = x_ntt + (((size_t)seg * 2 + part) * k + j) * N;
+    const uint32_t* ms = m_ntt + ((size_t)p * k + j) * N;
 #pragma unroll
     for (int e = 0; e < G_::E; ++e)
-      acc[e] = md.sub2p(acc[e] + mont_mul_lazy(ms[e], xs[e], inf.p, inf.pinv_neg));
+      acc[e] = md.sub2p(acc[e] + mont_mul_lazy(ms[row_index<LOGN, LE>(tid, e)], xs[row_index<LOGN, LE>(tid, e)], inf.p, inf.pinv_neg));
   }
   cta_inv<LOGN, LE, Mod32>(md, acc, sm, itw_all + (size_t)j * N, inf.ninv, inf.wn);
   uint32_t* dst = out + ((r * 2 + part) * k + j) * N;
@@ -649,18 +649,18 @@ __global__ void __launch_bounds__(Geo<LOGN, Loge32<LOGN>::v>::NT)
   __syncthreads();
   cta_fwd<LOGN, LE, Mod32>(md, xe, sm, tw_all + (size_t)j * N);
   const uint32_t g = gadget_i[j];
-  const size_t kofs = ((size_t)j * k + digit) * N + tid * G_::E;
-  const uint32_t* sj = s_ntt + (size_t)j * N + tid * G_::E;
-  const uint32_t* tj = target_ntt + (size_t)j * N + tid * G_::E;
+  const size_t kofs = ((size_t)j * k + digit) * N;
+  const uint32_t* sj = s_ntt + (size_t)j * N;
+  const uint32_t* tj = target_ntt + (size_t)j * N;
 #pragma unroll
   for (int e = 0; e < G_::E; ++e) {
     const uint32_t A = md.canon4(xa[e]);
     const uint32_t E = md.canon4(xe[e]);
-    const uint32_t as_e = addmod(mulmod_small(A, sj[e], inf), E, inf.p);
-    const uint32_t gt = mulmod_small(g, tj[e], inf);
+    const uint32_t as_e = addmod(mulmod_small(A, sj[row_index<LOGN, LE>(tid, e)], inf), E, inf.p);
+    const uint32_t gt = mulmod_small(g, tj[row_index<LOGN, LE>(tid, e)], inf);
     const uint32_t body = submod(gt, as_e, inf.p);
-    kbody[kofs + e] = mont_canon(body, inf);
-    kmask[kofs + e] = mont_canon(A, inf);
+    kbody[kofs + row_index<LOGN, LE>(tid, e)] = mont_canon(body, inf);
+    kmask[kofs + row_index<LOGN, LE>(tid, e)] = mont_canon(A, inf);
   }
 }
 

@@ -28,86 +28,117 @@ struct KsLoge {
   static constexpr int v = LOGN >= 14 ? 5 : 4;
 };
 
+// Ciphertexts handled per CTA: the forward twiddle table of the CTA's prime
+// is staged in shared memory once and reused for CH * k digit transforms.
+constexpr int KS_CTS_PER_CTA = 4;
+
+// Shared memory: Montgomery-form forward twiddles of prime j (N words), the
+// padded exchange tile, and the mask accumulator acc1 (N words, laid out
+// [register e][thread] so every thread touches its own conflict-free words).
+// The body accumulator acc0 and the digit being transformed stay in
+// registers (2 E words per thread).
 template <int LOGN, int LOGE>
-__global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT)
+__global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT,
+                                  Geo<LOGN, LOGE>::NT >= 512 ? 1 : 512 / Geo<LOGN, LOGE>::NT)
     k_keyswitch(const uint32_t* __restrict__ kbody, const uint32_t* __restrict__ kmask,
                 const uint32_t* __restrict__ digits, int64_t dig_stride, uint32_t* out0,
                 uint32_t* out1, int64_t out_stride, const int32_t* __restrict__ slot,
                 const uint32_t* __restrict__ adA0, const uint32_t* __restrict__ adA1,
                 int64_t adA_stride, const uint32_t* adB0, const uint32_t* adB1, int64_t adB_stride,
-                int k, const uint2* __restrict__ tw_all, const uint2* __restrict__ itw_all,
-                const Prime32Info* __restrict__ info) {
+                int64_t B, int k, const uint32_t* __restrict__ twm_all,
+                const uint2* __restrict__ itw_all, const Prime32Info* __restrict__ info) {
   typedef Geo<LOGN, LOGE> G_;
   constexpr int E = G_::E;
   constexpr int NT = G_::NT;
   constexpr int N = G_::N;
+  constexpr int R = G_::RLAST;
   extern __shared__ __align__(16) unsigned char smraw[];
-  uint32_t* sm = reinterpret_cast<uint32_t*>(smraw);
+  uint32_t* tws = reinterpret_cast<uint32_t*>(smraw);   // N forward twiddles (Montgomery)
+  uint32_t* sm = tws + N;                                // exchange tile
+  uint32_t* acc1s = sm + spad_size(N);                   // mask accumulator
   const int j = blockIdx.x;
-  const int64_t b = blockIdx.y;
   const int tid = threadIdx.x;
   const Prime32Info inf = info[j];
-  const Mod32 md = make_mod(inf);
-  const uint2* tw = tw_all + (size_t)j * N;
-  const uint32_t* dig = digits + b * dig_stride;
-
-  uint32_t acc0[E], acc1[E], x[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) acc0[e] = acc1[e] = 0u;
-
-  for (int i = 0; i < k; ++i) {
-    const uint32_t* src = dig + (size_t)i * N;
-#pragma unroll
-    for (int e = 0; e < E; ++e) x[e] = __ldg(src + tid + e * NT);
-    cta_fwd<LOGN, LOGE, Mod32>(md, x, sm, tw);
-    const size_t koff = ((size_t)j * k + i) * N + (size_t)tid * E;
-    const uint4* kb = reinterpret_cast<const uint4*>(kbody + koff);
-    const uint4* km = reinterpret_cast<const uint4*>(kmask + koff);
-#pragma unroll
-    for (int v = 0; v < E / 4; ++v) {
-      const uint4 wb = __ldg(kb + v);
-      const uint4 wm = __ldg(km + v);
-      const uint32_t bb[4] = {wb.x, wb.y, wb.z, wb.w};
-      const uint32_t mm[4] = {wm.x, wm.y, wm.z, wm.w};
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int e = v * 4 + q;
-        acc0[e] = md.sub2p(acc0[e] + mont_mul_lazy(x[e], bb[q], inf.p, inf.pinv_neg));
-        acc1[e] = md.sub2p(acc1[e] + mont_mul_lazy(x[e], mm[q], inf.p, inf.pinv_neg));
-      }
-    }
-  }
-
-  const int64_t s = slot ? (int64_t)slot[b] : b;
-  const uint2* itw = itw_all + (size_t)j * N;
-  // part 0
-  cta_inv<LOGN, LOGE, Mod32>(md, acc0, sm, itw, inf.ninv, inf.wn);
+  const Mod32M mm{inf.p, 2 * inf.p, inf.pinv};
+  const Mod32 md{inf.p, 2 * inf.p};
   {
-    uint32_t* o = out0 + s * out_stride + (size_t)j * N;
-    const uint32_t* a = adA0 ? adA0 + b * adA_stride + (size_t)j * N : nullptr;
-    const uint32_t* c = adB0 ? adB0 + s * adB_stride + (size_t)j * N : nullptr;
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int idx = tid + e * NT;
-      uint32_t v = md.subp(acc0[e]);
-      if (a) v = md.subp(v + a[idx]);
-      if (c) v = md.subp(v + c[idx]);
-      o[idx] = v;
-    }
+    const uint4* src = reinterpret_cast<const uint4*>(twm_all + (size_t)j * N);
+    uint4* dst = reinterpret_cast<uint4*>(tws);
+    for (int i = tid; i < N / 4; i += NT) dst[i] = __ldg(src + i);
   }
   __syncthreads();
-  cta_inv<LOGN, LOGE, Mod32>(md, acc1, sm, itw, inf.ninv, inf.wn);
-  {
-    uint32_t* o = out1 + s * out_stride + (size_t)j * N;
-    const uint32_t* a = adA1 ? adA1 + b * adA_stride + (size_t)j * N : nullptr;
-    const uint32_t* c = adB1 ? adB1 + s * adB_stride + (size_t)j * N : nullptr;
+  const uint2* itw = itw_all + (size_t)j * N;
+  const int64_t bbeg = (int64_t)blockIdx.y * KS_CTS_PER_CTA;
+  const int64_t bend = min(B, bbeg + KS_CTS_PER_CTA);
+
+  for (int64_t b = bbeg; b < bend; ++b) {
+    const uint32_t* dig = digits + b * dig_stride;
+    uint32_t acc0[E], x[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-      const int idx = tid + e * NT;
-      uint32_t v = md.subp(acc1[e]);
-      if (a) v = md.subp(v + a[idx]);
-      if (c) v = md.subp(v + c[idx]);
-      o[idx] = v;
+      acc0[e] = 0u;
+      acc1s[e * NT + tid] = 0u;
+    }
+
+    for (int i = 0; i < k; ++i) {
+      const uint32_t* src = dig + (size_t)i * N;
+#pragma unroll
+      for (int e = 0; e < E; ++e) x[e] = __ldg(src + tid + e * NT);
+      cta_fwd<LOGN, LOGE, Mod32M>(mm, x, sm, tws);
+      const size_t koff = ((size_t)j * k + i) * N;
+      if constexpr ((1 << R) >= 4) {
+#pragma unroll
+        for (int bb = 0; bb < G_::BLK; ++bb) {
+          const size_t o = koff + ((size_t)(bb * NT + tid) << R);
+          const uint4* kb = reinterpret_cast<const uint4*>(kbody + o);
+          const uint4* km = reinterpret_cast<const uint4*>(kmask + o);
+#pragma unroll
+          for (int v = 0; v < (1 << R) / 4; ++v) {
+            const uint4 wb = __ldg(kb + v);
+            const uint4 wm = __ldg(km + v);
+            const uint32_t kbv[4] = {wb.x, wb.y, wb.z, wb.w};
+            const uint32_t kmv[4] = {wm.x, wm.y, wm.z, wm.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int e = bb * (1 << R) + v * 4 + q;
+              acc0[e] = md.sub2p(acc0[e] + mont_mul_lazy(x[e], kbv[q], inf.p, inf.pinv_neg));
+              uint32_t& a1 = acc1s[e * NT + tid];
+              a1 = md.sub2p(a1 + mont_mul_lazy(x[e], kmv[q], inf.p, inf.pinv_neg));
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const size_t o = koff + row_index<LOGN, LOGE>(tid, e);
+          acc0[e] = md.sub2p(acc0[e] + mont_mul_lazy(x[e], __ldg(kbody + o), inf.p, inf.pinv_neg));
+          uint32_t& a1 = acc1s[e * NT + tid];
+          a1 = md.sub2p(a1 + mont_mul_lazy(x[e], __ldg(kmask + o), inf.p, inf.pinv_neg));
+        }
+      }
+    }
+
+    const int64_t s = slot ? (int64_t)slot[b] : b;
+#pragma unroll 1
+    for (int part = 0; part < 2; ++part) {
+      if (part == 1) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc0[e] = acc1s[e * NT + tid];
+      }
+      cta_inv<LOGN, LOGE, Mod32>(md, acc0, sm, itw, inf.ninv, inf.wn);
+      uint32_t* o = (part ? out1 : out0) + s * out_stride + (size_t)j * N;
+      const uint32_t* aA = part ? adA1 : adA0;
+      const uint32_t* aB = part ? adB1 : adB0;
+      const uint32_t* a = aA ? aA + b * adA_stride + (size_t)j * N : nullptr;
+      const uint32_t* c = aB ? aB + s * adB_stride + (size_t)j * N : nullptr;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int idx = tid + e * NT;
+        uint32_t v = md.subp(acc0[e]);
+        if (a) v = md.subp(v + a[idx]);
+        if (c) v = md.subp(v + c[idx]);
+        o[idx] = v;
+      }
     }
   }
 }
@@ -120,17 +151,18 @@ static int run_ks(hefv_ctx* c, const uint32_t* kb, const uint32_t* km, const uin
   constexpr int LE = KsLoge<LOGN>::v;
   typedef Geo<LOGN, LE> G_;
   auto kern = k_keyswitch<LOGN, LE>;
-  const size_t smem = (size_t)spad_size(G_::N) * 4;
+  const size_t smem = ((size_t)2 * G_::N + (size_t)spad_size(G_::N)) * 4;
   if (smem > 48 * 1024) {
     HEFV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   }
-  for (int64_t b0i = 0; b0i < B; b0i += 65535) {
-    const int64_t nb = (B - b0i) < 65535 ? (B - b0i) : 65535;
-    dim3 grid(c->k, (unsigned)nb);
+  const int64_t chunk = 65535ll * KS_CTS_PER_CTA;
+  for (int64_t b0i = 0; b0i < B; b0i += chunk) {
+    const int64_t nb = (B - b0i) < chunk ? (B - b0i) : chunk;
+    dim3 grid(c->k, (unsigned)((nb + KS_CTS_PER_CTA - 1) / KS_CTS_PER_CTA));
     kern<<<grid, G_::NT, smem, st>>>(kb, km, dig + b0i * ds, ds, o0, o1, os,
                                      slot ? slot + b0i : nullptr, a0 ? a0 + b0i * as : nullptr,
-                                     a1 ? a1 + b0i * as : nullptr, as, b0, b1, bs, c->k,
-                                     c->d_tw32, c->d_itw32, c->d_info32);
+                                     a1 ? a1 + b0i * as : nullptr, as, b0, b1, bs, nb, c->k,
+                                     c->d_twm32, c->d_itw32, c->d_info32);
     HEFV_LAUNCH_CHECK("k_keyswitch");
     if (!slot && nb < B) {
       // without a slot map the output index equals the batch index: shift bases

@@ -55,6 +55,31 @@ struct Mod32 {
   }
 };
 
+// Word-sized prime with single-word Montgomery-form twiddles (w * 2^32 mod p):
+// half the twiddle bytes of the Shoup pair, so a full forward table of a
+// 2^14-point transform fits in shared memory next to the data tile.
+struct Mod32M {
+  typedef uint32_t T;
+  typedef uint32_t Tw;
+  uint32_t p, p2, pinv;  // pinv = p^{-1} mod 2^32
+
+  // y * w * 2^-32 mod p in (0, 2p) for y < 2^32, w < p
+  __device__ __forceinline__ uint32_t mul(uint32_t y, uint32_t w) const {
+    const uint64_t t = (uint64_t)y * w;
+    const uint32_t m = (uint32_t)t * pinv;
+    return (uint32_t)(t >> 32) - __umulhi(m, p) + p;
+  }
+  __device__ __forceinline__ uint32_t sub2p(uint32_t x) const { return min(x, x - p2); }
+  __device__ __forceinline__ uint32_t subp(uint32_t x) const { return min(x, x - p); }
+  __device__ __forceinline__ uint32_t canon4(uint32_t x) const { return subp(sub2p(x)); }
+  __device__ __forceinline__ void ct(uint32_t& x, uint32_t& y, Tw w) const {
+    uint32_t a = sub2p(x);
+    uint32_t t = mul(y, w);
+    x = a + t;
+    y = a - t + p2;
+  }
+};
+
 // Montgomery REDC for a*b with b < p and a < 2^32: returns a*b*2^-32 mod p in [0, 2p).
 __device__ __forceinline__ uint32_t mont_mul_lazy(uint32_t a, uint32_t b, uint32_t p,
                                                   uint32_t pinv_neg) {
@@ -120,6 +145,8 @@ struct Prime32Info {
   uint64_t mu;        // floor(2^64 / p)
   uint2 ninv;         // (N^{-1}, shoup)
   uint2 wn;           // (psi_inv_rev[1] * N^{-1}, shoup)
+  uint32_t pinv;      // p^{-1} mod 2^32
+  uint32_t pad2;
 };
 
 struct Prime64Info {

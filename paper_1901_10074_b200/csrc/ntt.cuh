@@ -18,8 +18,9 @@
 // Register layouts (tid in [0, NT), NT = N / E):
 //   * "column" layout (pass 0 input, inverse output): element tid + e*NT.
 //     Global loads/stores in this layout are fully coalesced.
-//   * "row" layout (forward output, inverse input): element tid*E + e, i.e.
-//     E consecutive words per thread -> 128-bit vector loads/stores.
+//   * "row" layout (forward output, inverse input): row_index(tid, e) --
+//     blocks of 2^RLAST consecutive words, block b * NT + tid for register
+//     block b -> 128-bit vector loads/stores, conflict-free tile accesses.
 #pragma once
 #include "modarith.cuh"
 
@@ -38,6 +39,18 @@ struct Geo {
   static constexpr int BLK = E >> RLAST;                // last-pass blocks per thread
   static_assert(LOGN > LOGE || (LOGN == LOGE), "N must be >= E");
 };
+
+// Index of register e of thread tid in the "row" layout (forward output /
+// inverse input).  The last pass works on blocks of 2^RLAST consecutive
+// words; thread tid owns blocks b * NT + tid (b < BLK), so for a fixed
+// register consecutive threads touch consecutive blocks (conflict-free with
+// the padded tile, 16-byte vectorisable within a block).
+template <int LOGN, int LOGE>
+__device__ __forceinline__ int row_index(int tid, int e) {
+  typedef Geo<LOGN, LOGE> G_;
+  constexpr int R = G_::RLAST;
+  return ((((e >> R) * G_::NT) + tid) << R) | (e & ((1 << R) - 1));
+}
 
 // ---- forward (Cooley-Tukey, natural -> bit-reversed) ----------------------
 
@@ -72,7 +85,7 @@ __device__ __forceinline__ void fwd_last_pass(const M& md, typename M::T* x, int
   constexpr int s0 = LOGN - R;
 #pragma unroll
   for (int b = 0; b < G_::BLK; ++b) {
-    const int G = tid * G_::BLK + b;
+    const int G = b * G_::NT + tid;
     typename M::T* xb = x + b * (1 << R);
 #pragma unroll
     for (int l = 0; l < R; ++l) {
@@ -122,7 +135,7 @@ __device__ __forceinline__ void cta_fwd(const M& md, typename M::T* x, typename 
         x[e] = sm[spad(full_pass_index<LOGN, LOGE>(pass + 1, tid, e))];
     } else {
 #pragma unroll
-      for (int e = 0; e < G_::E; ++e) x[e] = sm[spad(tid * G_::E + e)];
+      for (int e = 0; e < G_::E; ++e) x[e] = sm[spad(row_index<LOGN, LOGE>(tid, e))];
     }
     __syncthreads();
   }
@@ -140,7 +153,7 @@ __device__ __forceinline__ void inv_last_pass(const M& md, typename M::T* x, int
   constexpr int s0 = LOGN - R;
 #pragma unroll
   for (int b = 0; b < G_::BLK; ++b) {
-    const int G = tid * G_::BLK + b;
+    const int G = b * G_::NT + tid;
     typename M::T* xb = x + b * (1 << R);
 #pragma unroll
     for (int l = R - 1; l >= 0; --l) {
@@ -207,7 +220,7 @@ __device__ __forceinline__ void cta_inv(const M& md, typename M::T* x, typename 
   for (int pass = G_::NFULL - 1; pass >= 0; --pass) {
     if (pass == G_::NFULL - 1) {
 #pragma unroll
-      for (int e = 0; e < G_::E; ++e) sm[spad(tid * G_::E + e)] = x[e];
+      for (int e = 0; e < G_::E; ++e) sm[spad(row_index<LOGN, LOGE>(tid, e))] = x[e];
     } else {
 #pragma unroll
       for (int e = 0; e < G_::E; ++e)
@@ -218,6 +231,31 @@ __device__ __forceinline__ void cta_inv(const M& md, typename M::T* x, typename 
     for (int e = 0; e < G_::E; ++e) x[e] = sm[spad(full_pass_index<LOGN, LOGE>(pass, tid, e))];
     __syncthreads();
     inv_full_pass<LOGN, LOGE, M>(md, x, pass, tid, itw, ninv, wn);
+  }
+}
+
+// Load / store E words of a row-layout stack (device NTT order) with 128-bit
+// accesses where the block length allows it.
+template <int LOGN, int LOGE>
+__device__ __forceinline__ void load_row(const uint32_t* __restrict__ base, int tid, uint32_t* v) {
+  typedef Geo<LOGN, LOGE> G_;
+  constexpr int R = G_::RLAST;
+  if constexpr ((1 << R) >= 4) {
+#pragma unroll
+    for (int b = 0; b < G_::BLK; ++b) {
+      const uint4* p = reinterpret_cast<const uint4*>(base + ((b * G_::NT + tid) << R));
+#pragma unroll
+      for (int q = 0; q < (1 << R) / 4; ++q) {
+        const uint4 w = __ldg(p + q);
+        v[b * (1 << R) + 4 * q + 0] = w.x;
+        v[b * (1 << R) + 4 * q + 1] = w.y;
+        v[b * (1 << R) + 4 * q + 2] = w.z;
+        v[b * (1 << R) + 4 * q + 3] = w.w;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < G_::E; ++e) v[e] = __ldg(base + row_index<LOGN, LOGE>(tid, e));
   }
 }
 

@@ -38,11 +38,11 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT)
   for (int e = 0; e < G_::E; ++e) x[e] = md.canon4(x[e]);
   if (!natural) {
 #pragma unroll
-    for (int e = 0; e < G_::E; ++e) dst[tid * G_::E + e] = x[e];
+    for (int e = 0; e < G_::E; ++e) dst[row_index<LOGN, LOGE>(tid, e)] = x[e];
   } else {
     // dev index i holds natural index bitrev(i): stage through smem
 #pragma unroll
-    for (int e = 0; e < G_::E; ++e) sm[spad(brev_n(tid * G_::E + e, LOGN))] = x[e];
+    for (int e = 0; e < G_::E; ++e) sm[spad(brev_n(row_index<LOGN, LOGE>(tid, e), LOGN))] = x[e];
     __syncthreads();
 #pragma unroll
     for (int e = 0; e < G_::E; ++e) dst[tid + e * G_::NT] = sm[spad(tid + e * G_::NT)];
@@ -69,14 +69,14 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT)
   T x[G_::E];
   if (!natural) {
 #pragma unroll
-    for (int e = 0; e < G_::E; ++e) x[e] = src[tid * G_::E + e];
+    for (int e = 0; e < G_::E; ++e) x[e] = src[row_index<LOGN, LOGE>(tid, e)];
   } else {
 #pragma unroll
     for (int e = 0; e < G_::E; ++e)
       sm[spad(brev_n(tid + e * G_::NT, LOGN))] = src[tid + e * G_::NT];
     __syncthreads();
 #pragma unroll
-    for (int e = 0; e < G_::E; ++e) x[e] = sm[spad(tid * G_::E + e)];
+    for (int e = 0; e < G_::E; ++e) x[e] = sm[spad(row_index<LOGN, LOGE>(tid, e))];
     __syncthreads();
   }
   cta_inv<LOGN, LOGE, M>(md, x, sm, itw, inf.ninv, inf.wn);
