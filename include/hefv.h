@@ -185,6 +185,12 @@ int hefv_accumulate_rows(hefv_ctx* ctx, const uint32_t* rows, const int32_t* seg
 int hefv_add_part0(hefv_ctx* ctx, uint32_t* rows, int64_t row_stride, const int32_t* slot,
                    const uint32_t* add, int64_t P, void* stream);
 
+/* ---- measurement ---------------------------------------------------------
+ * Integer-pipe throughput probe (roofline denominator; not a reference
+ * function): kind 0 IMAD, 1 IMAD.HI, 2 IMAD.WIDE, 3 IADD3, 4 Shoup butterfly;
+ * executes blocks * 256 * iters * 128 operations. */
+int hefv_probe_int(int32_t kind, int32_t blocks, int32_t iters, uint32_t* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

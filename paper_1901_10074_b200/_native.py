@@ -47,6 +47,7 @@ _SIGS = {
     "hefv_mult_tensor": [_P, _P, _P, _P, _P, _P],
     "hefv_accumulate_rows": [_P, _P, _P, _P, _P, _I32, _I32, _P],
     "hefv_add_part0": [_P, _P, _I64, _P, _P, _I64, _P],
+    "hefv_probe_int": [_I32, _I32, _I32, _P, _P],
 }
 
 EXPORTED = tuple(["hefv_last_error", "hefv_ctx_destroy"] + list(_SIGS))

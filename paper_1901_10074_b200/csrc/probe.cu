@@ -1,0 +1,86 @@
+// Integer-pipe peak probe.  MEASURED_PEAKS.json only carries HBM and bf16
+// figures; the NTT / key-switch roofline needs the integer multiply rates of
+// this part, so this kernel measures them (ops per second over the whole
+// GPU) for the instruction forms the transforms use:
+//   kind 0: IMAD      (32-bit multiply-add, low word)
+//   kind 1: IMAD.HI   (__umulhi)
+//   kind 2: IMAD.WIDE (32x32 -> 64-bit product)
+//   kind 3: IADD3     (ALU pipe reference)
+//   kind 4: one lazy Shoup Cooley-Tukey butterfly (counted as 1 op)
+// Each thread runs 8 independent chains so the pipes, not latency, bound it.
+#include "../../include/hefv.h"
+#include "internal.h"
+
+namespace hefv {
+
+template <int KIND>
+__global__ void __launch_bounds__(256) k_probe(uint32_t* out, int iters, uint32_t seed) {
+  uint32_t a[8], b[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    a[i] = seed * (threadIdx.x + 1) + i * 0x9e3779b9u;
+    b[i] = (seed ^ (blockIdx.x * 131u + i)) | 1u;
+  }
+  const uint32_t p = 1073692673u, p2 = 2u * p;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (KIND == 0) {
+          a[i] = a[i] * b[i] + 0x1234567u;
+        } else if (KIND == 1) {
+          a[i] = __umulhi(a[i], b[i]) ^ b[i];
+        } else if (KIND == 2) {
+          const uint64_t t = (uint64_t)a[i] * b[i];
+          a[i] = (uint32_t)t ^ (uint32_t)(t >> 32);
+        } else if (KIND == 3) {
+          a[i] = a[i] + b[i] + 0x777u;
+        } else {
+          // x = a[i], y = b[i] butterfly with twiddle (w, wsh)
+          const uint32_t w = 123456789u, wsh = 493903u;
+          uint32_t x = min(a[i], a[i] - p2);
+          const uint32_t q = __umulhi(b[i], wsh);
+          const uint32_t t = b[i] * w - q * p;
+          a[i] = x + t;
+          b[i] = x - t + p2;
+        }
+      }
+    }
+  }
+  uint32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s ^= a[i] ^ b[i];
+  if (s == 0x12345678u) out[0] = s;  // keep the work alive
+}
+
+}  // namespace hefv
+
+using namespace hefv;
+
+// ops executed = blocks * 256 threads * iters * 16 * 8
+extern "C" int hefv_probe_int(int32_t kind, int32_t blocks, int32_t iters, uint32_t* out,
+                              void* stream) {
+  cudaStream_t st = as_stream(stream);
+  switch (kind) {
+    case 0:
+      k_probe<0><<<blocks, 256, 0, st>>>(out, iters, 7u);
+      break;
+    case 1:
+      k_probe<1><<<blocks, 256, 0, st>>>(out, iters, 7u);
+      break;
+    case 2:
+      k_probe<2><<<blocks, 256, 0, st>>>(out, iters, 7u);
+      break;
+    case 3:
+      k_probe<3><<<blocks, 256, 0, st>>>(out, iters, 7u);
+      break;
+    case 4:
+      k_probe<4><<<blocks, 256, 0, st>>>(out, iters, 7u);
+      break;
+    default:
+      return fail("hefv_probe_int: unknown kind");
+  }
+  HEFV_LAUNCH_CHECK("k_probe");
+  return 0;
+}
