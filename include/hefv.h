@@ -35,6 +35,8 @@ typedef struct hefv_ctx hefv_ctx;
 /* ---- housekeeping ------------------------------------------------------ */
 const char* hefv_last_error(void);
 int hefv_abi_version(void);
+/* Number of kernels this library has launched (all contexts, process-wide). */
+uint64_t hefv_launch_count(void);
 
 /* Context: NTT tables for a set of word-sized primes (2^28 < p < 2^30) and a
  * set of 64-bit primes (p < 2^62), ring dimension N = 2^log_n.

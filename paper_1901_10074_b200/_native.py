@@ -50,7 +50,10 @@ _SIGS = {
     "hefv_probe_int": [_I32, _I32, _I32, _P, _P],
 }
 
-EXPORTED = tuple(["hefv_last_error", "hefv_ctx_destroy"] + list(_SIGS))
+EXPORTED = tuple(["hefv_last_error", "hefv_ctx_destroy", "hefv_launch_count"] + list(_SIGS))
+
+# host<->device byte accounting of the Python side (bench.py's e2e fields)
+TRAFFIC = {"h2d": 0, "d2h": 0}
 
 _lib = None
 
@@ -73,6 +76,8 @@ def load(require_cuda: bool = True):
     lib.hefv_last_error.argtypes = []
     lib.hefv_ctx_destroy.restype = None
     lib.hefv_ctx_destroy.argtypes = [_P]
+    lib.hefv_launch_count.restype = C.c_uint64
+    lib.hefv_launch_count.argtypes = []
     for name, args in _SIGS.items():
         fn = getattr(lib, name)
         fn.restype = C.c_int
@@ -91,6 +96,26 @@ def call(name: str, *args):
     """Invoke a status-returning ABI function and raise on error."""
     lib = load()
     check(getattr(lib, name)(*args), name)
+
+
+def launch_count() -> int:
+    return int(load().hefv_launch_count())
+
+
+def to_device(arr):
+    """numpy -> CUDA tensor (counted as host-to-device traffic)."""
+    import numpy as np
+    import torch
+
+    a = np.ascontiguousarray(arr)
+    TRAFFIC["h2d"] += a.nbytes
+    return torch.from_numpy(a).cuda()
+
+
+def to_host(t):
+    """CUDA tensor -> numpy (counted as device-to-host traffic)."""
+    TRAFFIC["d2h"] += t.numel() * t.element_size()
+    return t.cpu().numpy()
 
 
 def ptr(t) -> int | None:

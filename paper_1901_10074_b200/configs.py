@@ -92,3 +92,31 @@ def centred_mod(values, t: int) -> list:
         r = int(v) % t
         out.append(r - t if r > t // 2 else r)
     return out
+
+
+def workload_op_counts(cfg: int, data_seed=None) -> dict:
+    """Exact serial op counts of one encrypted inference of a config
+    (encryption of the input, every layer, decryption of the logits),
+    computed on the host from the compiled layers -- no FV arithmetic."""
+    from .inference import SquareSpec, compile_conv, compile_fc
+    from .planner import count_layer_ops
+
+    params = config_params(cfg)
+    img, net = config_network(cfg, data_seed)
+    s = params.slot_count
+    pow2 = {1 << j for j in range((s - 1).bit_length())}
+    length = int(np.prod(img.shape))
+    k_cur = -(-length // s)
+    tot = {"cmult": 0, "add": 0, "rotation": 0, "encrypt": k_cur, "mult": 0, "ks_hops": 0}
+    for layer in net.layers:
+        if isinstance(layer, SquareSpec):
+            tot["mult"] += k_cur
+            tot["ks_hops"] += k_cur  # one relinearisation per ct x ct product
+            continue
+        rows = compile_conv(layer, s) if isinstance(layer, ConvSpec) else compile_fc(layer, s)
+        c = count_layer_ops(rows, k_cur, s, s, pow2)
+        for key, v in c.items():
+            tot[key] += v
+        k_cur = max(1, -(-len(rows) // s))
+    tot["decrypt"] = k_cur
+    return tot

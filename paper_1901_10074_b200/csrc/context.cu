@@ -6,6 +6,7 @@
 // laid out for the merged-psi transforms in ntt.cuh: entry i of the forward
 // table is psi^bitrev(i) (with its Shoup companion), entry i of the inverse
 // table psi^-bitrev(i).
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -16,6 +17,9 @@
 namespace hefv {
 
 static thread_local std::string g_err;
+static std::atomic<uint64_t> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const std::string& msg) { g_err = msg; }
 int fail(const std::string& msg) {
@@ -88,6 +92,7 @@ extern "C" {
 
 const char* hefv_last_error(void) { return g_err.c_str(); }
 int hefv_abi_version(void) { return 1; }
+uint64_t hefv_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int hefv_ctx_create(hefv_ctx** out, uint32_t log_n, int32_t n32, const uint32_t* primes32,
                     const uint32_t* psi32, int32_t n64, const uint64_t* primes64,

@@ -49,6 +49,7 @@ struct hefv_ctx {
 };
 
 namespace hefv {
+void count_launch();
 void set_error(const std::string& msg);
 int fail(const std::string& msg);
 int check_cuda(cudaError_t e, const char* where);
@@ -63,6 +64,7 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 #define HEFV_LAUNCH_CHECK(where)                                            \
   do {                                                                      \
+    hefv::count_launch();                                                   \
     cudaError_t _e = cudaGetLastError();                                    \
     if (_e != cudaSuccess) return hefv::check_cuda(_e, where);              \
   } while (0)

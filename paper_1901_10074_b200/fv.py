@@ -139,7 +139,7 @@ class FvContext:
             "hefv_fv_setup")
         # gadget_i mod q_j table (k x k)
         gtab = np.array([[g % p for p in self.q_primes] for g in self.gadget], dtype=np.int64)
-        self.d_gadget = torch.from_numpy(gtab.astype(np.int32)).cuda()
+        self.d_gadget = nat.to_device(gtab.astype(np.int32))
         self.p_col = np.array(self.q_primes, dtype=np.int64)[:, None]
         self.brev = bitrev_perm(self.log_n)
         self._ntt_cache = {}
@@ -208,7 +208,7 @@ class FvContext:
         """(B, N) signed small ints -> (B, k, N) NTT (device order)."""
         torch = _torch()
         s = np.asarray(small, dtype=np.int8).reshape(-1, self.n)
-        d = torch.from_numpy(s).cuda()
+        d = nat.to_device(s)
         out = self.empty(s.shape[0], self.k, self.n)
         self.call("hefv_small_to_rns", d.data_ptr(), out.data_ptr(), s.shape[0], 1,
                   1 if montgomery else 0, self.stream())
@@ -216,8 +216,7 @@ class FvContext:
 
     def upload_residues(self, arr: np.ndarray):
         torch = _torch()
-        return torch.from_numpy(np.ascontiguousarray(np.asarray(arr, dtype=np.int64)
-                                                     .astype(np.int32))).cuda()
+        return nat.to_device(np.asarray(arr, dtype=np.int64).astype(np.int32))
 
     def ntt_q(self, stacks, inverse=False, natural=False):
         """In-device transform of (B, k, N) stacks under the q primes."""
@@ -244,7 +243,7 @@ class FvContext:
 
     def dev_to_natural(self, stacks_dev_order) -> np.ndarray:
         """Host copy of device-order NTT stacks in the reference's natural order."""
-        host = stacks_dev_order.cpu().numpy().astype(np.int64)
+        host = nat.to_host(stacks_dev_order).astype(np.int64)
         out = np.empty_like(host)
         out[..., self.brev] = host
         return out
@@ -272,7 +271,7 @@ class SwitchKey:
         ctx = self._ctx
         torch = _torch()
         # undo Montgomery form: x * 2^-32 == mont(x, 1) -- do it on the host exactly
-        host = dev.cpu().numpy().astype(np.int64)
+        host = nat.to_host(dev).astype(np.int64)
         out = []
         for j, p in enumerate(ctx.q_primes):
             rinv = pow(1 << 32, -1, p)
@@ -314,7 +313,7 @@ class KeySet:
         if "public" not in self._cache:
             ctx = self.context
             coeff = ctx.ntt_q(self.pk_ntt.contiguous(), inverse=True)
-            host = coeff.cpu().numpy().astype(np.int64)
+            host = nat.to_host(coeff).astype(np.int64)
             self._cache["public"] = (host[0], host[1])
         return self._cache["public"]
 
@@ -330,8 +329,8 @@ def _switch_key(ctx: FvContext, s_ntt, target_ntt, rng) -> SwitchKey:
     for i in range(k):
         a = ctx.rand_uniform(rng)
         e = ctx.rand_error(rng)
-        a_d = torch.from_numpy(a.astype(np.int32)).cuda()
-        e_d = torch.from_numpy(e.astype(np.int8)).cuda()
+        a_d = nat.to_device(a.astype(np.int32))
+        e_d = nat.to_device(e.astype(np.int8))
         ctx.call("hefv_keygen_digit", a_d.data_ptr(), e_d.data_ptr(), i,
                  ctx.d_gadget[i].data_ptr(), s_ntt.data_ptr(), target_ntt.data_ptr(),
                  body.data_ptr(), mask.data_ptr(), st)
@@ -386,7 +385,7 @@ class FvCiphertext:
     @property
     def parts(self):
         if self._host is None:
-            host = self._dev.cpu().numpy().astype(np.int64)
+            host = nat.to_host(self._dev).astype(np.int64)
             self._host = [host[i] for i in range(host.shape[0])]
         return self._host
 
@@ -399,7 +398,7 @@ class FvCiphertext:
         if self._dev is None:
             torch = _torch()
             stack = np.stack(self._host).astype(np.int32)
-            self._dev = torch.from_numpy(stack).cuda()
+            self._dev = nat.to_device(stack)
         return self._dev
 
     @property
@@ -442,7 +441,7 @@ class FvBackend(SlotBackend):
         arr = np.asarray(vecs)
         arr = np.array(arr.tolist(), dtype=np.uint64) if arr.dtype == object else arr.astype(np.uint64)
         arr = arr.reshape(-1, self.ctx.n // 2)
-        return torch.from_numpy(arr.view(np.int64)).cuda()
+        return nat.to_device(arr.view(np.int64))
 
     def _encode_dev(self, vecs):
         """(B, N/2) slot vectors -> (B, N) plaintext polys mod t (device)."""
@@ -458,7 +457,7 @@ class FvBackend(SlotBackend):
         return out
 
     def _host_plain(self, dev) -> np.ndarray:
-        arr = dev.cpu().numpy()
+        arr = nat.to_host(dev)
         return arr if self.ctx.t < (1 << 31) else arr.astype(object)
 
     def encode(self, vec) -> np.ndarray:
@@ -473,7 +472,7 @@ class FvBackend(SlotBackend):
         p = np.asarray(poly)
         p = np.array([int(x) % t for x in p], dtype=np.uint64) if p.dtype == object else \
             np.mod(p.astype(np.int64), t).astype(np.uint64)
-        dev = _torch().from_numpy(p.view(np.int64).reshape(1, -1)).cuda()
+        dev = nat.to_device(p.view(np.int64).reshape(1, -1))
         return self._host_plain(self._decode_dev(dev)[0])
 
     def _rns_plain(self, polys, mode, to_ntt, montgomery):
@@ -521,7 +520,7 @@ class FvBackend(SlotBackend):
             e2[b] = ctx.rand_error(self.rng)
         dm = self._delta_m_dev(np.stack([np.asarray(v) for v in vecs]))
         out = ctx.empty(B, 2, ctx.k, ctx.n)
-        ud, e1d, e2d = (torch.from_numpy(x).cuda() for x in (u, e1, e2))
+        ud, e1d, e2d = (nat.to_device(x) for x in (u, e1, e2))
         ctx.call("hefv_encrypt", self._pk_mont.data_ptr(), ud.data_ptr(), e1d.data_ptr(),
                  e2d.data_ptr(), dm.data_ptr(), out.data_ptr(), B, ctx.stream())
         return [self._fresh(out[b], 0) for b in range(B)]
@@ -558,7 +557,7 @@ class FvBackend(SlotBackend):
         res = [None] * len(cts)
         for _, idx in groups.items():
             slots = self._decode_dev(self._decrypt_poly_dev([cts[i].device() for i in idx]))
-            host = slots.cpu().numpy()
+            host = nat.to_host(slots)
             for r, i in enumerate(idx):
                 res[i] = np.asarray(host[r] if self.ctx.t < (1 << 31) else host[r].astype(object),
                                     dtype=self._dtype)
@@ -596,14 +595,14 @@ class FvBackend(SlotBackend):
         return self._relinearize(out3, level)
 
     def _relinearize(self, out3, level):
+        from .planner import keyswitch_call
+
         ctx = self.ctx
         out = ctx.empty(2, ctx.k, ctx.n)
         key = self.keys.relin
-        stack = ctx.k * ctx.n
-        ctx.call("hefv_keyswitch", key.body_dev.data_ptr(), key.mask_dev.data_ptr(),
-                 out3[2].data_ptr(), 0, out[0].data_ptr(), out[1].data_ptr(), 0, None,
-                 out3[0].data_ptr(), out3[1].data_ptr(), 0, None, None, 0, 1, ctx.stream())
-        del stack
+        keyswitch_call(ctx, key.body_dev.data_ptr(), key.mask_dev.data_ptr(), out3[2].data_ptr(),
+                       0, out[0].data_ptr(), out[1].data_ptr(), 0, None, out3[0].data_ptr(),
+                       out3[1].data_ptr(), 0, None, None, 0, 1)
         return self._fresh(out, level)
 
     def rotation_hops(self, offset: int) -> list:
@@ -620,11 +619,13 @@ class FvBackend(SlotBackend):
         scratch = ctx.empty(2, ctx.k, ctx.n)
         ctx.call("hefv_automorph", dev.data_ptr(), 0, None, scratch.data_ptr(), 2, g, 1,
                  ctx.stream())
+        from .planner import keyswitch_call
+
         out = ctx.empty(2, ctx.k, ctx.n)
         key = self.keys.galois[off]
-        ctx.call("hefv_keyswitch", key.body_dev.data_ptr(), key.mask_dev.data_ptr(),
-                 scratch[1].data_ptr(), 0, out[0].data_ptr(), out[1].data_ptr(), 0, None,
-                 scratch[0].data_ptr(), None, 0, None, None, 0, 1, ctx.stream())
+        keyswitch_call(ctx, key.body_dev.data_ptr(), key.mask_dev.data_ptr(), scratch[1].data_ptr(),
+                       0, out[0].data_ptr(), out[1].data_ptr(), 0, None, scratch[0].data_ptr(),
+                       None, 0, None, None, 0, 1)
         return out
 
     def _rotate(self, a, offset, level):

@@ -35,10 +35,67 @@ from __future__ import annotations
 
 import numpy as np
 
+from . import _native as nat
 from .errors import DepthBudgetError
 from .ring import galois_element
 
 _TILE_BYTES = 24 << 30  # device memory budget for one tile's working set
+
+# Instrumentation read by bench.py: key-switch launches / ciphertexts, and
+# (when KS_EVENTS is a list) CUDA event pairs bracketing every key-switch
+# launch on the launching stream.
+STATS = {"ks_launches": 0, "ks_cts": 0}
+KS_EVENTS = None
+
+
+def keyswitch_call(ctx, *args):
+    """hefv_keyswitch through the context, with the planner's accounting.
+    The batch size is the second-to-last argument."""
+    import torch
+
+    batch = int(args[-1])
+    STATS["ks_launches"] += 1
+    STATS["ks_cts"] += batch
+    if KS_EVENTS is not None:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        ctx.call("hefv_keyswitch", *args, ctx.stream())
+        e1.record()
+        KS_EVENTS.append((e0, e1, batch))
+    else:
+        ctx.call("hefv_keyswitch", *args, ctx.stream())
+
+
+def count_layer_ops(rows, x_k: int, s: int, slot_count: int, galois_offsets,
+                    skip_zero_segments=True) -> dict:
+    """Exact op counts of the serial schedule for one compiled layer
+    (inference.py:277-349), plus the key-switch hops its rotations cost."""
+    n_iter = _allsum_iters(s)
+    tot = {"cmult": 0, "add": 0, "rotation": 0, "encrypt": 0, "ks_hops": 0}
+    seen, biased_only = set(), set()
+    for r in rows:
+        nseg = len(r.segment_ids) if skip_zero_segments else x_k
+        m, off = divmod(r.out_index, s)
+        if nseg == 0:
+            if r.bias:
+                biased_only.add(m)
+            continue
+        counts, _, _ = _row_events(nseg, n_iter, bool(r.bias), bool(off), m not in seen)
+        seen.add(m)
+        for f, v in counts.items():
+            tot[f] += v
+        tot["ks_hops"] += n_iter
+        if off:
+            rot = (-off) % slot_count
+            tot["ks_hops"] += 1 if rot in galois_offsets else bin(rot).count("1")
+    nout = max(1, -(-len(rows) // s))
+    for m in range(nout):
+        if m not in seen:
+            tot["encrypt"] += 1
+        elif m in biased_only:
+            tot["add"] += 1
+    return tot
 
 
 # ---------------------------------------------------------------------------
@@ -250,17 +307,17 @@ def _run_rows(backend, rows, x, seg_lists, active, m_arr, off_arr, bias_arr, out
         P = len(plain_seg)
         acc = torch.empty((B, 2, kq, n), dtype=torch.int32, device="cuda")
         if P:
-            d_ptr = torch.tensor(ptr, dtype=torch.int32, device="cuda")
-            d_idx = torch.from_numpy(np.concatenate(slot_idx).astype(np.int32)).cuda()
-            d_val = torch.from_numpy(np.concatenate(vals).view(np.int64)).cuda()
+            d_ptr = nat.to_device(np.asarray(ptr, dtype=np.int32))
+            d_idx = nat.to_device(np.concatenate(slot_idx).astype(np.int32))
+            d_val = nat.to_device(np.concatenate(vals).view(np.int64))
             polys = torch.empty((P, n), dtype=torch.int64, device="cuda")
             ctx.call("hefv_encode_sparse", d_ptr.data_ptr(), d_idx.data_ptr(), d_val.data_ptr(),
                      polys.data_ptr(), P, st)
             m_ntt = torch.empty((P, kq, n), dtype=torch.int32, device="cuda")
             ctx.call("hefv_plain_to_rns", polys.data_ptr(), m_ntt.data_ptr(), P, 1, 1, 0, st)
             del polys
-            d_rp = torch.tensor(row_ptr, dtype=torch.int32, device="cuda")
-            d_ps = torch.tensor(plain_seg, dtype=torch.int32, device="cuda")
+            d_rp = nat.to_device(np.asarray(row_ptr, dtype=np.int32))
+            d_ps = nat.to_device(np.asarray(plain_seg, dtype=np.int32))
             ctx.call("hefv_rows_mac", x_ntt.data_ptr(), m_ntt.data_ptr(), d_rp.data_ptr(),
                      d_ps.data_ptr(), acc.data_ptr(), B, st)
             del m_ntt
@@ -277,8 +334,8 @@ def _run_rows(backend, rows, x, seg_lists, active, m_arr, off_arr, bias_arr, out
             key = keys[shift]
             g = galois_element(shift, n)
             ctx.call("hefv_automorph", a0, ct_words, None, s0, 2, g, B, st)
-            ctx.call("hefv_keyswitch", key.body_dev.data_ptr(), key.mask_dev.data_ptr(), s1,
-                     ct_words, a0, a1, ct_words, None, s0, None, ct_words, a0, a1, ct_words, B, st)
+            keyswitch_call(ctx, key.body_dev.data_ptr(), key.mask_dev.data_ptr(), s1, ct_words,
+                           a0, a1, ct_words, None, s0, None, ct_words, a0, a1, ct_words, B)
         # ---- 4. biases and the e0 mask ---------------------------------------------
         bias_rows = [bi for bi, i in enumerate(tile) if bias_arr[i]]
         if bias_rows:
@@ -286,13 +343,13 @@ def _run_rows(backend, rows, x, seg_lists, active, m_arr, off_arr, bias_arr, out
             d_ptr = torch.arange(nb + 1, dtype=torch.int32, device="cuda")
             d_idx = torch.zeros(nb, dtype=torch.int32, device="cuda")
             bv = np.array([bias_arr[tile[bi]] % t for bi in bias_rows], dtype=np.uint64)
-            d_val = torch.from_numpy(bv.view(np.int64)).cuda()
+            d_val = nat.to_device(bv.view(np.int64))
             polys = torch.empty((nb, n), dtype=torch.int64, device="cuda")
             ctx.call("hefv_encode_sparse", d_ptr.data_ptr(), d_idx.data_ptr(), d_val.data_ptr(),
                      polys.data_ptr(), nb, st)
             dm = torch.empty((nb, kq, n), dtype=torch.int32, device="cuda")
             ctx.call("hefv_plain_to_rns", polys.data_ptr(), dm.data_ptr(), nb, 0, 0, 0, st)
-            d_slot = torch.tensor(bias_rows, dtype=torch.int32, device="cuda")
+            d_slot = nat.to_device(np.asarray(bias_rows, dtype=np.int32))
             ctx.call("hefv_add_part0", a0, ct_words, d_slot.data_ptr(), dm.data_ptr(), nb, st)
         ctx.call("hefv_mul_plain", a0, e0.data_ptr(), a0, B, 2, 1, st)
         # ---- 5. placement rotations by -off ------------------------------------------
@@ -307,24 +364,24 @@ def _run_rows(backend, rows, x, seg_lists, active, m_arr, off_arr, bias_arr, out
         # custom (non power-of-two) keys are single hops; power-of-two hops ascend
         for h in sorted(hop_groups, key=lambda v: (v & (v - 1) == 0, v)):
             idx = hop_groups[h]
-            d_slot = torch.tensor(idx, dtype=torch.int32, device="cuda")
+            d_slot = nat.to_device(np.asarray(idx, dtype=np.int32))
             nb = len(idx)
             sub = scr[:nb]
             b0 = sub.data_ptr()
             key = keys[h]
             ctx.call("hefv_automorph", a0, ct_words, d_slot.data_ptr(), b0, 2,
                      galois_element(h, n), nb, st)
-            ctx.call("hefv_keyswitch", key.body_dev.data_ptr(), key.mask_dev.data_ptr(),
-                     b0 + stack * 4, ct_words, a0, a1, ct_words, d_slot.data_ptr(), b0, None,
-                     ct_words, None, None, 0, nb, st)
+            keyswitch_call(ctx, key.body_dev.data_ptr(), key.mask_dev.data_ptr(),
+                           b0 + stack * 4, ct_words, a0, a1, ct_words, d_slot.data_ptr(), b0, None,
+                           ct_words, None, None, 0, nb)
         del scr
         # ---- 6. sum pieces into their output ciphertexts -----------------------------
         ms = m_arr[tile]
         bounds = np.flatnonzero(np.diff(ms)) + 1
         seg = np.concatenate([[0], bounds, [B]]).astype(np.int32)
         seg_out = ms[seg[:-1]].astype(np.int32)
-        d_seg = torch.from_numpy(seg).cuda()
-        d_out = torch.from_numpy(seg_out).cuda()
+        d_seg = nat.to_device(seg)
+        d_out = nat.to_device(seg_out)
         ctx.call("hefv_accumulate_rows", a0, d_seg.data_ptr(), d_out.data_ptr(),
                  out_dev.data_ptr(), len(seg_out), 1, st)
         del acc
