@@ -27,6 +27,21 @@ struct InfoOf<Mod64> {
 __device__ __forceinline__ int brev_n(int x, int logn) { return (int)(__brev((unsigned)x) >> (32 - logn)); }
 
 
+// Streaming loads that do not allocate in L1 (keys, digits): L1 is kept for
+// the twiddle tables that every CTA of the same prime re-reads.
+__device__ __forceinline__ uint4 ld_stream_v4(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p) {
+  uint32_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+
 // LOGE (log2 words per thread) used by the CTA-resident 32-bit transforms.
 template <int LOGN>
 struct Loge32 {

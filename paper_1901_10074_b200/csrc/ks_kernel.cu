@@ -25,7 +25,7 @@ namespace hefv {
 
 template <int LOGN>
 struct KsLoge {
-  static constexpr int v = LOGN >= 14 ? 5 : 4;
+  static constexpr int v = LOGN >= 15 ? 5 : 4;
 };
 
 // Ciphertexts handled per CTA: the forward twiddle table of the CTA's prime
@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT,
                 uint32_t* out1, int64_t out_stride, const int32_t* __restrict__ slot,
                 const uint32_t* __restrict__ adA0, const uint32_t* __restrict__ adA1,
                 int64_t adA_stride, const uint32_t* adB0, const uint32_t* adB1, int64_t adB_stride,
-                int64_t B, int k, const uint32_t* __restrict__ twm_all,
+                int64_t B, int k, const uint2* __restrict__ tw_all,
                 const uint2* __restrict__ itw_all, const Prime32Info* __restrict__ info) {
   typedef Geo<LOGN, LOGE> G_;
   constexpr int E = G_::E;
@@ -53,18 +53,21 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT,
   constexpr int N = G_::N;
   constexpr int R = G_::RLAST;
   extern __shared__ __align__(16) unsigned char smraw[];
-  uint32_t* tws = reinterpret_cast<uint32_t*>(smraw);   // N forward twiddles (Montgomery)
-  uint32_t* sm = tws + N;                                // exchange tile
-  uint32_t* acc1s = sm + spad_size(N);                   // mask accumulator
+  // Shoup twiddles of the full passes ([1, 2^(LOGN-RLAST))) in shared
+  // memory; the last pass reads its N - 2^(LOGN-RLAST) entries through L1.
+  constexpr int NTW = 1 << (LOGN - R);
+  uint2* tws = reinterpret_cast<uint2*>(smraw);
+  uint32_t* sm = reinterpret_cast<uint32_t*>(tws + NTW);  // exchange tile
+  uint32_t* acc1s = sm + spad_size(N);                    // mask accumulator
   const int j = blockIdx.x;
   const int tid = threadIdx.x;
   const Prime32Info inf = info[j];
-  const Mod32M mm{inf.p, 2 * inf.p, inf.pinv};
   const Mod32 md{inf.p, 2 * inf.p};
+  const uint2* twg = tw_all + (size_t)j * N;
   {
-    const uint4* src = reinterpret_cast<const uint4*>(twm_all + (size_t)j * N);
+    const uint4* src = reinterpret_cast<const uint4*>(twg);
     uint4* dst = reinterpret_cast<uint4*>(tws);
-    for (int i = tid; i < N / 4; i += NT) dst[i] = __ldg(src + i);
+    for (int i = tid; i < NTW / 2; i += NT) dst[i] = __ldg(src + i);
   }
   __syncthreads();
   const uint2* itw = itw_all + (size_t)j * N;
@@ -83,8 +86,8 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT,
     for (int i = 0; i < k; ++i) {
       const uint32_t* src = dig + (size_t)i * N;
 #pragma unroll
-      for (int e = 0; e < E; ++e) x[e] = __ldg(src + tid + e * NT);
-      cta_fwd<LOGN, LOGE, Mod32M>(mm, x, sm, tws);
+      for (int e = 0; e < E; ++e) x[e] = ld_stream(src + tid + e * NT);
+      cta_fwd<LOGN, LOGE, Mod32>(md, x, sm, tws, twg);
       const size_t koff = ((size_t)j * k + i) * N;
       if constexpr ((1 << R) >= 4) {
 #pragma unroll
@@ -94,8 +97,8 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT,
           const uint4* km = reinterpret_cast<const uint4*>(kmask + o);
 #pragma unroll
           for (int v = 0; v < (1 << R) / 4; ++v) {
-            const uint4 wb = __ldg(kb + v);
-            const uint4 wm = __ldg(km + v);
+            const uint4 wb = ld_stream_v4(kb + v);
+            const uint4 wm = ld_stream_v4(km + v);
             const uint32_t kbv[4] = {wb.x, wb.y, wb.z, wb.w};
             const uint32_t kmv[4] = {wm.x, wm.y, wm.z, wm.w};
 #pragma unroll
@@ -151,7 +154,8 @@ static int run_ks(hefv_ctx* c, const uint32_t* kb, const uint32_t* km, const uin
   constexpr int LE = KsLoge<LOGN>::v;
   typedef Geo<LOGN, LE> G_;
   auto kern = k_keyswitch<LOGN, LE>;
-  const size_t smem = ((size_t)2 * G_::N + (size_t)spad_size(G_::N)) * 4;
+  const size_t smem = (size_t)(1 << (LOGN - G_::RLAST)) * sizeof(uint2) +
+                      ((size_t)G_::N + (size_t)spad_size(G_::N)) * 4;
   if (smem > 48 * 1024) {
     HEFV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   }
@@ -162,7 +166,7 @@ static int run_ks(hefv_ctx* c, const uint32_t* kb, const uint32_t* km, const uin
     kern<<<grid, G_::NT, smem, st>>>(kb, km, dig + b0i * ds, ds, o0, o1, os,
                                      slot ? slot + b0i : nullptr, a0 ? a0 + b0i * as : nullptr,
                                      a1 ? a1 + b0i * as : nullptr, as, b0, b1, bs, nb, c->k,
-                                     c->d_twm32, c->d_itw32, c->d_info32);
+                                     c->d_tw32, c->d_itw32, c->d_info32);
     HEFV_LAUNCH_CHECK("k_keyswitch");
     if (!slot && nb < B) {
       // without a slot map the output index equals the batch index: shift bases

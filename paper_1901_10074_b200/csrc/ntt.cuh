@@ -119,7 +119,8 @@ __device__ __forceinline__ int full_pass_index(int pass, int tid, int e) {
 // spad_size(N) words.  Caller must __syncthreads() before reusing `sm`.
 template <int LOGN, int LOGE, class M>
 __device__ __forceinline__ void cta_fwd(const M& md, typename M::T* x, typename M::T* sm,
-                                        const typename M::Tw* __restrict__ tw) {
+                                        const typename M::Tw* __restrict__ tw,
+                                        const typename M::Tw* __restrict__ tw_last = nullptr) {
   typedef Geo<LOGN, LOGE> G_;
   const int tid = threadIdx.x;
 #pragma unroll
@@ -139,7 +140,7 @@ __device__ __forceinline__ void cta_fwd(const M& md, typename M::T* x, typename 
     }
     __syncthreads();
   }
-  fwd_last_pass<LOGN, LOGE, M>(md, x, tid, tw);
+  fwd_last_pass<LOGN, LOGE, M>(md, x, tid, tw_last ? tw_last : tw);
 }
 
 // ---- inverse (Gentleman-Sande, bit-reversed -> natural) -------------------
