@@ -113,13 +113,14 @@ def _barrier(world):
         dist.barrier()
 
 
-def _max_over_ranks(value, world):
+def _max_over_ranks(value, world, device="cuda"):
+    """Max of a per-rank timing over all ranks (NCCL on the GPU, gloo in tests)."""
     if world == 1:
         return value
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    t = torch.tensor([value], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 

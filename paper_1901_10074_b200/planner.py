@@ -156,6 +156,26 @@ def _row_events(nseg: int, n_iter: int, has_bias: bool, has_off: bool, first: bo
 # ---------------------------------------------------------------------------
 # the planner
 # ---------------------------------------------------------------------------
+def replay_ledger(ledger, rows, x_k, s, width, n_iter, m_arr, off_arr, bias_arr, nseg,
+                  row_level):
+    """Apply the serial schedule's ledger events for a layer, in row order.
+    Returns (output ciphertexts that receive pieces, bias-only plaintexts)."""
+    seen_m = set()
+    plain_bias = {}
+    for i in range(len(rows)):
+        m = int(m_arr[i])
+        if not nseg[i]:
+            if bias_arr[i]:
+                plain_bias.setdefault(m, np.zeros(width, dtype=np.int64))[int(off_arr[i])] += bias_arr[i]
+            continue
+        first = m not in seen_m
+        seen_m.add(m)
+        counts, dlive, peak = _row_events(int(nseg[i]), n_iter, bool(bias_arr[i]),
+                                          bool(off_arr[i]), first)
+        ledger.absorb(counts, dlive, peak, int(row_level[i]) + 1)
+    return seen_m, plain_bias
+
+
 def _allsum_iters(s: int) -> int:
     n, shift = 0, 1
     while shift < s:
@@ -198,23 +218,9 @@ def planned_layer_eval(backend, rows, x, skip_zero_segments=True, scale_factor=1
             raise DepthBudgetError(f"operation needs level {bad} but depth_budget is {budget}")
         row_level[i] = lv
 
-    # ledger replay, in row order
-    seen_m = set()
-    ledger_max = 0
-    plain_bias = {}
-    for i in range(R):
-        m = int(m_arr[i])
-        if not has_acc[i]:
-            if bias_arr[i]:
-                plain_bias.setdefault(m, np.zeros(width, dtype=np.int64))[int(off_arr[i])] += bias_arr[i]
-            continue
-        first = m not in seen_m
-        seen_m.add(m)
-        counts, dlive, peak = _row_events(int(nseg[i]), n_iter, bool(bias_arr[i]),
-                                          bool(off_arr[i]), first)
-        lv = int(row_level[i]) + 1
-        backend._c.absorb(counts, dlive, peak, lv)
-        ledger_max = max(ledger_max, lv)
+    seen_m, plain_bias = replay_ledger(backend._c, rows, x_k=x.k, s=s, width=width,
+                                       n_iter=n_iter, m_arr=m_arr, off_arr=off_arr,
+                                       bias_arr=bias_arr, nseg=nseg, row_level=row_level)
 
     # ---- device work ------------------------------------------------------------
     active = np.nonzero(has_acc)[0]
