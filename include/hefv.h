@@ -39,7 +39,8 @@ int hefv_abi_version(void);
 uint64_t hefv_launch_count(void);
 
 /* Context: NTT tables for a set of word-sized primes (2^28 < p < 2^30) and a
- * set of 64-bit primes (p < 2^62), ring dimension N = 2^log_n.
+ * set of 64-bit primes (p < 2^62), ring dimension N = 2^log_n, 1 <= log_n <= 16
+ * (the FV entry points need 4 <= log_n <= 14).
  * Replaces NttPrime.__init__ (ntt.py:149-172) for every prime of
  * _FvContext.__init__ (fv.py:83, fv.py:95, fv.py:101).  psi is the primitive
  * 2N-th root the reference picks (g^((p-1)/2N), g the smallest generator). */

@@ -99,7 +99,7 @@ int hefv_ctx_create(hefv_ctx** out, uint32_t log_n, int32_t n32, const uint32_t*
                     const uint64_t* psi64) {
   if (!out) return fail("hefv_ctx_create: null out pointer");
   *out = nullptr;
-  if (log_n < 4 || log_n > 16) return fail("hefv_ctx_create: log_n must be in [4, 16]");
+  if (log_n < 1 || log_n > 16) return fail("hefv_ctx_create: log_n must be in [1, 16]");
   if (n32 < 0 || n64 < 0 || n32 + n64 == 0) return fail("hefv_ctx_create: empty prime set");
   hefv_ctx* c = new hefv_ctx();
   c->log_n = (int)log_n;

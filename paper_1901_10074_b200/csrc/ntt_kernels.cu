@@ -114,6 +114,12 @@ static int dispatch(int log_n, bool fwd, const typename M::T* in, typename M::T*
   case L:            \
     return launch_one<L, 4, M>(fwd, in, out, batch, nprimes, prime_base, natural, tw, info, st);
   switch (log_n) {
+    case 1:
+      return launch_one<1, 1, M>(fwd, in, out, batch, nprimes, prime_base, natural, tw, info, st);
+    case 2:
+      return launch_one<2, 2, M>(fwd, in, out, batch, nprimes, prime_base, natural, tw, info, st);
+    case 3:
+      return launch_one<3, 3, M>(fwd, in, out, batch, nprimes, prime_base, natural, tw, info, st);
     HEFV_CASE(4)
     HEFV_CASE(5)
     HEFV_CASE(6)

@@ -31,8 +31,8 @@ class NttPrime:
 
         if (p - 1) % (2 * n) != 0:
             raise ValueError(f"p={p} is not 1 mod {2 * n}")
-        if n < 16 or n > 1 << 16 or n & (n - 1):
-            raise ValueError("ring dimension must be a power of two in [16, 65536]")
+        if n < 2 or n > 1 << 16 or n & (n - 1):
+            raise ValueError("ring dimension must be a power of two in [2, 65536]")
         if p >= _U64_LIMIT:
             raise ValueError("primes must be below 2^62")
         nat.require_device()

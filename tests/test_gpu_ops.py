@@ -5,6 +5,8 @@ tests/test_oracle.py; here the CUDA path (through the C-ABI) must produce
 the same ciphertext limbs under the same seeded keys and randomness.
 """
 
+import json
+
 import numpy as np
 import pytest
 
@@ -163,3 +165,58 @@ def test_tiny_params_all_ops(rng):
     for g, o in [(gpu.mult(ga, ga), orc.mult(oa, oa)), (gpu.rotate(ga, 7), orc.rotate(oa, 7)),
                  (gpu.cmult(ga, v), orc.cmult(oa, v))]:
         assert _digest(g.parts) == _digest(o.parts)
+
+
+def test_desk_golden_replay_matches_reference():
+    """The reference's own desk run (seed 77, 10 ops) replayed on the GPU."""
+    import json
+    from pathlib import Path
+
+    from paper_1901_10074_b200.fv import FvBackend
+    from goldens import replay_ops
+
+    g = json.loads((Path(__file__).resolve().parent / "golden" / "fv_desk.json").read_text())
+    be = FvBackend(profile("desk"), rng=np.random.default_rng(g["seed"]))
+    k = be.keys
+    assert O.limb_digest([k.secret]) == g["secret"]
+    assert O.limb_digest(list(k.public)) == g["pk"]
+    assert O.limb_digest(list(k.relin.body) + list(k.relin.mask)) == g["relin"]
+    for off, d in g["galois"].items():
+        sk = k.galois[int(off)]
+        assert O.limb_digest(list(sk.body) + list(sk.mask)) == d, off
+    got, want = replay_ops(be, g)
+    for key, val in got.items():
+        assert val == want[key], key
+
+
+def test_tiny_golden_full_limbs():
+    import json
+    from pathlib import Path
+
+    from paper_1901_10074_b200.fv import FvBackend
+
+    g = json.loads((Path(__file__).resolve().parent / "golden" / "fv_tiny.json").read_text())
+    p = BackendParams(**g["params"])
+    be = FvBackend(p, rng=np.random.default_rng(g["key_seed"]))
+    v = np.random.default_rng(g["data_seed"]).integers(0, 257, 32)
+    a = be.encrypt(v)
+    assert [x.tolist() for x in a.parts] == g["enc"]
+    assert [x.tolist() for x in be.mult(a, a).parts] == g["square"]
+    assert [x.tolist() for x in be.rotate(a, 7).parts] == g["rotate7"]
+    assert [x.tolist() for x in be.cmult(a, v).parts] == g["cmult"]
+
+
+@pytest.mark.parametrize("case", json.loads((__import__("pathlib").Path(__file__).resolve().parent
+                                             / "golden" / "ntt.json").read_text())["cases"],
+                         ids=lambda c: f"n{c['n']}b{c['bits']}")
+def test_ntt_golden_vectors(case):
+    from paper_1901_10074_b200.ntt import NttPrime
+
+    n, p = case["n"], case["p"]
+    tr = NttPrime(p, n)
+    assert tr.psi == case["psi"]
+    rng = np.random.default_rng(case["seed"])
+    a = np.array([int(rng.integers(0, p)) for _ in range(n)], dtype=object)
+    fa = tr.fwd(a)
+    assert O.limb_digest([np.asarray([int(x) for x in fa], dtype=np.int64)]) == case["fwd_digest"]
+    assert [int(x) for x in tr.inv(fa)] == [int(x) for x in a]
