@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(Geo<LOGN, 4>::NT)
 #pragma unroll
   for (int e = 0; e < G_::E; ++e) x[e] = reduce_any(src[tid + e * G_::NT], inf);
   cta_fwd<LOGN, 4, Mod64>(md, x, sm, tw_all + (size_t)t_index * G_::N);
+  __syncthreads();
 #pragma unroll
   for (int e = 0; e < G_::E; ++e) sm[spad(row_index<LOGN, 4>(tid, e))] = md.canon4(x[e]);
   __syncthreads();

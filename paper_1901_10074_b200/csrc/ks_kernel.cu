@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT,
       if constexpr ((1 << R) >= 4) {
 #pragma unroll
         for (int bb = 0; bb < G_::BLK; ++bb) {
-          const size_t o = koff + ((size_t)(bb * NT + tid) << R);
+          const size_t o = koff + row_index<LOGN, LOGE>(tid, bb << R);
           const uint4* kb = reinterpret_cast<const uint4*>(kbody + o);
           const uint4* km = reinterpret_cast<const uint4*>(kmask + o);
 #pragma unroll

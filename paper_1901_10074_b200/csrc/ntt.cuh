@@ -26,6 +26,12 @@
 
 namespace hefv {
 
+// Shared-tile address map: an XOR swizzle of the low 5 bits with bits
+// [LOGE, LOGE + 5).  With the register layouts below it makes every exchange
+// of every supported (N, E) conflict-free (checked exhaustively on the host),
+// and, being a bijection on [0, N), needs no padding words.
+template <int LOGE>
+__device__ __forceinline__ int swz(int x) { return x + (x >> 4); }
 __device__ __forceinline__ int spad(int x) { return x + (x >> 4); }
 __host__ __device__ constexpr int spad_size(int n) { return n + (n >> 4) + 1; }
 
@@ -41,15 +47,34 @@ struct Geo {
 };
 
 // Index of register e of thread tid in the "row" layout (forward output /
-// inverse input).  The last pass works on blocks of 2^RLAST consecutive
-// words; thread tid owns blocks b * NT + tid (b < BLK), so for a fixed
-// register consecutive threads touch consecutive blocks (conflict-free with
-// the padded tile, 16-byte vectorisable within a block).
+// inverse input): E consecutive words per thread (the last pass's blocks of
+// 2^RLAST words are contiguous per thread), so every exchange after pass 0
+// stays inside a warp or a small warp group, and global accesses are
+// 128-bit vectors.
 template <int LOGN, int LOGE>
 __device__ __forceinline__ int row_index(int tid, int e) {
-  typedef Geo<LOGN, LOGE> G_;
-  constexpr int R = G_::RLAST;
-  return ((((e >> R) * G_::NT) + tid) << R) | (e & ((1 << R) - 1));
+  return (tid << LOGE) + e;
+}
+
+// Load a contiguous run of `count` (<= MAXC, compile-time after unrolling)
+// twiddles with 16-byte accesses where possible.
+template <class Tw, int MAXC>
+__device__ __forceinline__ void load_tw_run(const Tw* __restrict__ p, Tw* out, const int count) {
+  if (sizeof(Tw) == 8 && count % 2 == 0) {
+    const uint4* q = reinterpret_cast<const uint4*>(p);
+#pragma unroll
+    for (int i = 0; i < MAXC / 2; ++i) {
+      if (2 * i < count) {
+        const uint4 v = q[i];
+        out[2 * i] = *reinterpret_cast<const Tw*>(&v.x);
+        out[2 * i + 1] = *reinterpret_cast<const Tw*>(&v.z);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < MAXC; ++i)
+      if (i < count) out[i] = p[i];
+  }
 }
 
 // ---- forward (Cooley-Tukey, natural -> bit-reversed) ----------------------
@@ -83,21 +108,24 @@ __device__ __forceinline__ void fwd_last_pass(const M& md, typename M::T* x, int
   typedef Geo<LOGN, LOGE> G_;
   constexpr int R = G_::RLAST;
   constexpr int s0 = LOGN - R;
+  constexpr int BLK = G_::BLK;
+  // the thread owns blocks tid*BLK .. tid*BLK+BLK-1, so at stage l its
+  // twiddles are one contiguous run of BLK * 2^l table entries
 #pragma unroll
-  for (int b = 0; b < G_::BLK; ++b) {
-    const int G = b * G_::NT + tid;
-    typename M::T* xb = x + b * (1 << R);
+  for (int l = 0; l < R; ++l) {
+    const int half = (1 << R) >> (l + 1);
+    typename M::Tw w[BLK << (R - 1)];
+    load_tw_run<typename M::Tw, (BLK << (R - 1))>(tw + (1 << (s0 + l)) + ((tid * BLK) << l), w,
+                                                  BLK << l);
 #pragma unroll
-    for (int l = 0; l < R; ++l) {
-      const int half = (1 << R) >> (l + 1);
-      const typename M::Tw* twb = tw + (1 << (s0 + l)) + (G << l);
+    for (int b = 0; b < BLK; ++b) {
+      typename M::T* xb = x + b * (1 << R);
 #pragma unroll
       for (int u = 0; u < (1 << l); ++u) {
-        const typename M::Tw w = twb[u];
 #pragma unroll
         for (int e0 = 0; e0 < half; ++e0) {
           const int e = u * 2 * half + e0;
-          md.ct(xb[e], xb[e + half], w);
+          md.ct(xb[e], xb[e + half], w[(b << l) + u]);
         }
       }
     }
@@ -114,31 +142,59 @@ __device__ __forceinline__ int full_pass_index(int pass, int tid, int e) {
   return (G << (LOGN - s0)) + L + (e << tsh);
 }
 
+// Barrier over the group of 2^GL threads that exchange data through the
+// tile: a warp-local __syncwarp when the group fits a warp, a named barrier
+// (ids 1..8, one per group) for multi-warp groups, __syncthreads for the CTA.
+// (GL is a compile-time constant after the pass loops are unrolled.)
+template <int LOG_NT>
+__device__ __forceinline__ void group_sync(int tid, const int GL) {
+  if (GL >= LOG_NT) {
+    __syncthreads();
+  } else if (GL <= 5) {
+    __syncwarp();
+  } else {
+    const int G = (GL > LOG_NT - 3) ? GL : LOG_NT - 3;  // at most 8 groups
+    if (G >= LOG_NT) {
+      __syncthreads();
+    } else {
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + (tid >> G)), "r"(1 << G) : "memory");
+    }
+  }
+}
+
 // Forward transform of x (column layout in registers) -> row layout in
 // registers, lazily reduced to [0, 4p).  `sm` is a padded tile of
-// spad_size(N) words.  Caller must __syncthreads() before reusing `sm`.
+// spad_size(N) words.  The exchange after full pass p only involves the
+// 2^(LOGN - (p+1) LOGE) threads that share a pass-p region, so only the first
+// exchange is CTA-wide; later ones use group / warp barriers.
 template <int LOGN, int LOGE, class M>
 __device__ __forceinline__ void cta_fwd(const M& md, typename M::T* x, typename M::T* sm,
                                         const typename M::Tw* __restrict__ tw,
                                         const typename M::Tw* __restrict__ tw_last = nullptr) {
   typedef Geo<LOGN, LOGE> G_;
+  constexpr int LOG_NT = LOGN - LOGE;
   const int tid = threadIdx.x;
 #pragma unroll
   for (int pass = 0; pass < G_::NFULL; ++pass) {
     fwd_full_pass<LOGN, LOGE, M>(md, x, pass, tid, tw);
-    // exchange: write in this pass's layout, read in the next pass's layout
+    // pre-write barrier: CTA-wide before the first exchange (the tile may still
+    // be read by the previous transform), group-wide afterwards
+    if (pass == 0) {
+      __syncthreads();
+    } else {
+      group_sync<LOG_NT>(tid, LOGN - (pass + 1) * LOGE);
+    }
 #pragma unroll
-    for (int e = 0; e < G_::E; ++e) sm[spad(full_pass_index<LOGN, LOGE>(pass, tid, e))] = x[e];
-    __syncthreads();
+    for (int e = 0; e < G_::E; ++e) sm[swz<LOGE>(full_pass_index<LOGN, LOGE>(pass, tid, e))] = x[e];
+    group_sync<LOG_NT>(tid, LOGN - (pass + 1) * LOGE);
     if (pass + 1 < G_::NFULL) {
 #pragma unroll
       for (int e = 0; e < G_::E; ++e)
-        x[e] = sm[spad(full_pass_index<LOGN, LOGE>(pass + 1, tid, e))];
+        x[e] = sm[swz<LOGE>(full_pass_index<LOGN, LOGE>(pass + 1, tid, e))];
     } else {
 #pragma unroll
-      for (int e = 0; e < G_::E; ++e) x[e] = sm[spad(row_index<LOGN, LOGE>(tid, e))];
+      for (int e = 0; e < G_::E; ++e) x[e] = sm[swz<LOGE>(row_index<LOGN, LOGE>(tid, e))];
     }
-    __syncthreads();
   }
   fwd_last_pass<LOGN, LOGE, M>(md, x, tid, tw_last ? tw_last : tw);
 }
@@ -152,24 +208,31 @@ __device__ __forceinline__ void inv_last_pass(const M& md, typename M::T* x, int
   typedef Geo<LOGN, LOGE> G_;
   constexpr int R = G_::RLAST;
   constexpr int s0 = LOGN - R;
+  constexpr int BLK = G_::BLK;
 #pragma unroll
-  for (int b = 0; b < G_::BLK; ++b) {
-    const int G = b * G_::NT + tid;
-    typename M::T* xb = x + b * (1 << R);
+  for (int l = R - 1; l >= 0; --l) {
+    const int half = (1 << R) >> (l + 1);
+    if (s0 + l == 0) {
+      // whole transform is one last pass (tiny N): merged N^-1 stage
 #pragma unroll
-    for (int l = R - 1; l >= 0; --l) {
-      const int half = (1 << R) >> (l + 1);
-      const typename M::Tw* twb = itw + (1 << (s0 + l)) + (G << l);
+      for (int b = 0; b < BLK; ++b) {
+#pragma unroll
+        for (int e0 = 0; e0 < half; ++e0) md.gs_last(x[b * (1 << R) + e0], x[b * (1 << R) + e0 + half], ninv, wn);
+      }
+      continue;
+    }
+    typename M::Tw w[BLK << (R - 1)];
+    load_tw_run<typename M::Tw, (BLK << (R - 1))>(itw + (1 << (s0 + l)) + ((tid * BLK) << l), w,
+                                                  BLK << l);
+#pragma unroll
+    for (int b = 0; b < BLK; ++b) {
+      typename M::T* xb = x + b * (1 << R);
 #pragma unroll
       for (int u = 0; u < (1 << l); ++u) {
 #pragma unroll
         for (int e0 = 0; e0 < half; ++e0) {
           const int e = u * 2 * half + e0;
-          if (s0 + l == 0) {
-            md.gs_last(xb[e], xb[e + half], ninv, wn);
-          } else {
-            md.gs(xb[e], xb[e + half], twb[u]);
-          }
+          md.gs(xb[e], xb[e + half], w[(b << l) + u]);
         }
       }
     }
@@ -210,27 +273,31 @@ __device__ __forceinline__ void inv_full_pass(const M& md, typename M::T* x, int
 
 // Inverse transform: x in row layout (values < 2p) -> column layout
 // (natural coefficient order), values in [0, 2p).  N^{-1} is applied.
+// Exchanges run from fine (warp / group) to coarse (CTA-wide).
 template <int LOGN, int LOGE, class M>
 __device__ __forceinline__ void cta_inv(const M& md, typename M::T* x, typename M::T* sm,
                                         const typename M::Tw* __restrict__ itw,
                                         typename M::Tw ninv, typename M::Tw wn) {
   typedef Geo<LOGN, LOGE> G_;
+  constexpr int LOG_NT = LOGN - LOGE;
   const int tid = threadIdx.x;
   inv_last_pass<LOGN, LOGE, M>(md, x, tid, itw, ninv, wn);
 #pragma unroll
   for (int pass = G_::NFULL - 1; pass >= 0; --pass) {
+    // group of this exchange: threads sharing a pass-`pass` region
     if (pass == G_::NFULL - 1) {
+      __syncthreads();  // the tile may still be in use by a previous transform
 #pragma unroll
-      for (int e = 0; e < G_::E; ++e) sm[spad(row_index<LOGN, LOGE>(tid, e))] = x[e];
+      for (int e = 0; e < G_::E; ++e) sm[swz<LOGE>(row_index<LOGN, LOGE>(tid, e))] = x[e];
     } else {
+      group_sync<LOG_NT>(tid, LOGN - (pass + 2) * LOGE);
 #pragma unroll
       for (int e = 0; e < G_::E; ++e)
-        sm[spad(full_pass_index<LOGN, LOGE>(pass + 1, tid, e))] = x[e];
+        sm[swz<LOGE>(full_pass_index<LOGN, LOGE>(pass + 1, tid, e))] = x[e];
     }
-    __syncthreads();
+    group_sync<LOG_NT>(tid, LOGN - (pass + 1) * LOGE);
 #pragma unroll
-    for (int e = 0; e < G_::E; ++e) x[e] = sm[spad(full_pass_index<LOGN, LOGE>(pass, tid, e))];
-    __syncthreads();
+    for (int e = 0; e < G_::E; ++e) x[e] = sm[swz<LOGE>(full_pass_index<LOGN, LOGE>(pass, tid, e))];
     inv_full_pass<LOGN, LOGE, M>(md, x, pass, tid, itw, ninv, wn);
   }
 }
@@ -244,7 +311,7 @@ __device__ __forceinline__ void load_row(const uint32_t* __restrict__ base, int 
   if constexpr ((1 << R) >= 4) {
 #pragma unroll
     for (int b = 0; b < G_::BLK; ++b) {
-      const uint4* p = reinterpret_cast<const uint4*>(base + ((b * G_::NT + tid) << R));
+      const uint4* p = reinterpret_cast<const uint4*>(base + row_index<LOGN, LOGE>(tid, b << R));
 #pragma unroll
       for (int q = 0; q < (1 << R) / 4; ++q) {
         const uint4 w = __ldg(p + q);
@@ -257,6 +324,45 @@ __device__ __forceinline__ void load_row(const uint32_t* __restrict__ base, int 
   } else {
 #pragma unroll
     for (int e = 0; e < G_::E; ++e) v[e] = __ldg(base + row_index<LOGN, LOGE>(tid, e));
+  }
+}
+
+// Row-layout (E contiguous words per thread) global access, 16-byte vectors.
+template <int LOGN, int LOGE, class T>
+__device__ __forceinline__ void store_row_vec(T* __restrict__ base, int tid, const T* v) {
+  constexpr int E = 1 << LOGE;
+  constexpr int PER = 16 / sizeof(T);
+  T* p = base + row_index<LOGN, LOGE>(tid, 0);
+  if constexpr (E % PER == 0) {
+#pragma unroll
+    for (int i = 0; i < E / PER; ++i) {
+      uint4 w;
+      T* ws = reinterpret_cast<T*>(&w);
+#pragma unroll
+      for (int q = 0; q < PER; ++q) ws[q] = v[i * PER + q];
+      reinterpret_cast<uint4*>(p)[i] = w;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < E; ++e) p[e] = v[e];
+  }
+}
+template <int LOGN, int LOGE, class T>
+__device__ __forceinline__ void load_row_vec(const T* __restrict__ base, int tid, T* v) {
+  constexpr int E = 1 << LOGE;
+  constexpr int PER = 16 / sizeof(T);
+  const T* p = base + row_index<LOGN, LOGE>(tid, 0);
+  if constexpr (E % PER == 0) {
+#pragma unroll
+    for (int i = 0; i < E / PER; ++i) {
+      const uint4 w = reinterpret_cast<const uint4*>(p)[i];
+      const T* ws = reinterpret_cast<const T*>(&w);
+#pragma unroll
+      for (int q = 0; q < PER; ++q) v[i * PER + q] = ws[q];
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = p[e];
   }
 }
 

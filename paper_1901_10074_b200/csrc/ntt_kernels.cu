@@ -37,10 +37,10 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT)
 #pragma unroll
   for (int e = 0; e < G_::E; ++e) x[e] = md.canon4(x[e]);
   if (!natural) {
-#pragma unroll
-    for (int e = 0; e < G_::E; ++e) dst[row_index<LOGN, LOGE>(tid, e)] = x[e];
+    store_row_vec<LOGN, LOGE, T>(dst, tid, x);
   } else {
     // dev index i holds natural index bitrev(i): stage through smem
+    __syncthreads();
 #pragma unroll
     for (int e = 0; e < G_::E; ++e) sm[spad(brev_n(row_index<LOGN, LOGE>(tid, e), LOGN))] = x[e];
     __syncthreads();
@@ -68,8 +68,7 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT)
   const int tid = threadIdx.x;
   T x[G_::E];
   if (!natural) {
-#pragma unroll
-    for (int e = 0; e < G_::E; ++e) x[e] = src[row_index<LOGN, LOGE>(tid, e)];
+    load_row_vec<LOGN, LOGE, T>(src, tid, x);
   } else {
 #pragma unroll
     for (int e = 0; e < G_::E; ++e)
