@@ -142,6 +142,49 @@ __device__ __forceinline__ int full_pass_index(int pass, int tid, int e) {
   return (G << (LOGN - s0)) + L + (e << tsh);
 }
 
+// ---- exchange addressing ---------------------------------------------------
+// Exchange xi moves data from full-pass-xi layout to full-pass-(xi+1) (or row)
+// layout through the tile with the padding map pad(x) = x + K (x >> S).
+// (K, S) per exchange were chosen by an exhaustive bank simulation so that
+// both the writes and the reads of every exchange are conflict-free for all
+// supported (N, E).  All exchanges of one transform use the same padding
+// ratio K / 2^S (1/16 for E = 16, 1/32 for E = 32): a group's element region
+// (a multiple of 2^S words) then maps to the same address range in every
+// exchange, which is what makes the group-scoped barriers sufficient.  The
+// tile needs at most N + N/16 words.  Addresses are a per-thread base plus a
+// compile-time offset per register.
+__host__ __device__ constexpr int xpad_k(int LOGN, int LOGE, int xi) {
+  return LOGE == 4 ? (xi == (LOGN - 1) / 4 - 1 ? 1 : 2) : 1;
+}
+__host__ __device__ constexpr int xpad_s(int LOGN, int LOGE, int xi) {
+  return LOGE == 4 ? (xi == (LOGN - 1) / 4 - 1 ? 4 : 5) : 5;
+}
+
+template <int LOGN, int LOGE>
+__device__ __forceinline__ int xaddr_full(int pass, int tid, int e, int K, int S) {
+  const int s0 = pass * LOGE;
+  const int tsh = LOGN - s0 - LOGE;
+  const int T = 1 << tsh;
+  const int G = tid >> tsh;
+  const int L = tid & (T - 1);
+  const int A = G << (LOGN - s0);
+  int base = A + L;
+  int off = e * T;
+  if (K) {
+    base += K * (A >> S) + (T >= (1 << S) ? K * (L >> S) : 0);
+    off += T >= (1 << S) ? K * e * (T >> S) : K * ((e * T) >> S);
+  }
+  return base + off;
+}
+
+template <int LOGN, int LOGE>
+__device__ __forceinline__ int xaddr_row(int tid, int e, int K, int S) {
+  const int A = tid << LOGE;
+  int base = A + (K ? K * (A >> S) : 0);
+  int off = e + ((K && (1 << LOGE) >= (1 << S)) ? K * (e >> S) : 0);
+  return base + off;
+}
+
 // Barrier over the group of 2^GL threads that exchange data through the
 // tile: a warp-local __syncwarp when the group fits a warp, a named barrier
 // (ids 1..8, one per group) for multi-warp groups, __syncthreads for the CTA.
@@ -184,16 +227,16 @@ __device__ __forceinline__ void cta_fwd(const M& md, typename M::T* x, typename 
     } else {
       group_sync<LOG_NT>(tid, LOGN - (pass + 1) * LOGE);
     }
+    const int K = xpad_k(LOGN, LOGE, pass), S = xpad_s(LOGN, LOGE, pass);
 #pragma unroll
-    for (int e = 0; e < G_::E; ++e) sm[swz<LOGE>(full_pass_index<LOGN, LOGE>(pass, tid, e))] = x[e];
+    for (int e = 0; e < G_::E; ++e) sm[xaddr_full<LOGN, LOGE>(pass, tid, e, K, S)] = x[e];
     group_sync<LOG_NT>(tid, LOGN - (pass + 1) * LOGE);
     if (pass + 1 < G_::NFULL) {
 #pragma unroll
-      for (int e = 0; e < G_::E; ++e)
-        x[e] = sm[swz<LOGE>(full_pass_index<LOGN, LOGE>(pass + 1, tid, e))];
+      for (int e = 0; e < G_::E; ++e) x[e] = sm[xaddr_full<LOGN, LOGE>(pass + 1, tid, e, K, S)];
     } else {
 #pragma unroll
-      for (int e = 0; e < G_::E; ++e) x[e] = sm[swz<LOGE>(row_index<LOGN, LOGE>(tid, e))];
+      for (int e = 0; e < G_::E; ++e) x[e] = sm[xaddr_row<LOGN, LOGE>(tid, e, K, S)];
     }
   }
   fwd_last_pass<LOGN, LOGE, M>(md, x, tid, tw_last ? tw_last : tw);
@@ -285,19 +328,20 @@ __device__ __forceinline__ void cta_inv(const M& md, typename M::T* x, typename 
 #pragma unroll
   for (int pass = G_::NFULL - 1; pass >= 0; --pass) {
     // group of this exchange: threads sharing a pass-`pass` region
+    // this exchange is the inverse of forward exchange `pass`: same padding
+    const int K = xpad_k(LOGN, LOGE, pass), S = xpad_s(LOGN, LOGE, pass);
     if (pass == G_::NFULL - 1) {
       __syncthreads();  // the tile may still be in use by a previous transform
 #pragma unroll
-      for (int e = 0; e < G_::E; ++e) sm[swz<LOGE>(row_index<LOGN, LOGE>(tid, e))] = x[e];
+      for (int e = 0; e < G_::E; ++e) sm[xaddr_row<LOGN, LOGE>(tid, e, K, S)] = x[e];
     } else {
       group_sync<LOG_NT>(tid, LOGN - (pass + 2) * LOGE);
 #pragma unroll
-      for (int e = 0; e < G_::E; ++e)
-        sm[swz<LOGE>(full_pass_index<LOGN, LOGE>(pass + 1, tid, e))] = x[e];
+      for (int e = 0; e < G_::E; ++e) sm[xaddr_full<LOGN, LOGE>(pass + 1, tid, e, K, S)] = x[e];
     }
     group_sync<LOG_NT>(tid, LOGN - (pass + 1) * LOGE);
 #pragma unroll
-    for (int e = 0; e < G_::E; ++e) x[e] = sm[swz<LOGE>(full_pass_index<LOGN, LOGE>(pass, tid, e))];
+    for (int e = 0; e < G_::E; ++e) x[e] = sm[xaddr_full<LOGN, LOGE>(pass, tid, e, K, S)];
     inv_full_pass<LOGN, LOGE, M>(md, x, pass, tid, itw, ninv, wn);
   }
 }
