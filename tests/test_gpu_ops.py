@@ -220,3 +220,80 @@ def test_ntt_golden_vectors(case):
     fa = tr.fwd(a)
     assert O.limb_digest([np.asarray([int(x) for x in fa], dtype=np.int64)]) == case["fwd_digest"]
     assert [int(x) for x in tr.inv(fa)] == [int(x) for x in a]
+
+
+# ---------------------------------------------------------------- race stress
+@pytest.mark.parametrize("log_n,bits", [(10, 30), (12, 30), (13, 30), (14, 30), (15, 30),
+                                        (12, 50), (14, 55)])
+def test_transform_roundtrip_stress(log_n, bits):
+    """Many CTAs, repeated: device-order forward then inverse must be the
+    identity bit for bit (catches exchange/barrier races)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1901_10074_b200 import _native as nat
+    from paper_1901_10074_b200.ring import root_of_unity
+
+    n = 1 << log_n
+    primes = O.ntt_primes(4, bits, 2 * n)
+    psis = [root_of_unity(p, n) for p in primes]
+    lib = nat.load()
+    h = C.c_void_p()
+    wide = bits > 30
+    if wide:
+        nat.check(lib.hefv_ctx_create(C.byref(h), log_n, 0, None, None, 4,
+                                      (C.c_uint64 * 4)(*primes), (C.c_uint64 * 4)(*psis)))
+        gen = torch.Generator(device="cuda").manual_seed(log_n)
+        x = torch.randint(0, 1 << 40, (64, 4, n), dtype=torch.int64, device="cuda", generator=gen)
+        x = x % torch.tensor(primes, dtype=torch.int64, device="cuda").view(1, 4, 1)
+        fwd, inv = lib.hefv_ntt_fwd64, lib.hefv_ntt_inv64
+    else:
+        nat.check(lib.hefv_ctx_create(C.byref(h), log_n, 4, (C.c_uint32 * 4)(*primes),
+                                      (C.c_uint32 * 4)(*psis), 0, None, None))
+        gen = torch.Generator(device="cuda").manual_seed(log_n)
+        x = torch.randint(0, 1 << 29, (64, 4, n), dtype=torch.int32, device="cuda", generator=gen)
+        fwd, inv = lib.hefv_ntt_fwd32, lib.hefv_ntt_inv32
+    y = torch.empty_like(x)
+    z = torch.empty_like(x)
+    st = torch.cuda.current_stream().cuda_stream
+    for _ in range(5):
+        nat.check(fwd(h, x.data_ptr(), y.data_ptr(), 64, 4, 0, 0, st))
+        nat.check(inv(h, y.data_ptr(), z.data_ptr(), 64, 4, 0, 0, st))
+        assert torch.equal(z, x)
+    lib.hefv_ctx_destroy(h)
+
+
+@pytest.mark.parametrize("name", ["desk", "retina"])
+def test_mul_plain_and_keyswitch_batch_stress(name):
+    import torch
+
+    from paper_1901_10074_b200.fv import FvBackend
+    from paper_1901_10074_b200.ring import galois_element
+
+    p = profile(name)
+    be = FvBackend(p, rng=np.random.default_rng(2))
+    ctx = be.ctx
+    k, n = ctx.k, ctx.n
+    stack = k * n
+    a = be.encrypt(np.arange(p.slot_count) % 11)
+    # NTT-domain constant 1 in Montgomery form (2^32 mod q_j at every point)
+    one = torch.tensor([[(1 << 32) % q] * n for q in ctx.q_primes], dtype=torch.int64)
+    one = one.to(torch.int32).view(1, k, n).cuda()
+    B = 64
+    acc = torch.stack([a.device()] * B).contiguous()
+    out = torch.empty_like(acc)
+    for _ in range(3):
+        ctx.call("hefv_mul_plain", acc.data_ptr(), one.data_ptr(), out.data_ptr(), B, 2, 1,
+                 ctx.stream())
+        assert torch.equal(out, acc)
+    scr = torch.empty_like(acc)
+    key = be.keys.galois[1]
+    ctx.call("hefv_automorph", acc.data_ptr(), 2 * stack, None, scr.data_ptr(), 2,
+             galois_element(1, n), B, ctx.stream())
+    ctx.call("hefv_keyswitch", key.body_dev.data_ptr(), key.mask_dev.data_ptr(),
+             scr.data_ptr() + stack * 4, 2 * stack, out.data_ptr(), out.data_ptr() + stack * 4,
+             2 * stack, None, scr.data_ptr(), None, 2 * stack, None, None, 0, B, ctx.stream())
+    single = be.rotate(a, 1).device()
+    for b in range(B):
+        assert torch.equal(out[b], single)
