@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT,
   constexpr int NTW = 1 << (LOGN - R);
   uint2* tws = reinterpret_cast<uint2*>(smraw);
   uint32_t* sm = reinterpret_cast<uint32_t*>(tws + NTW);  // exchange tile
-  uint32_t* acc1s = sm + spad_size(N);                    // mask accumulator
+  uint32_t* acc1s = sm + ((spad_size(N) + 3) & ~3);      // mask accumulator (16B aligned)
   const int j = blockIdx.x;
   const int tid = threadIdx.x;
   const Prime32Info inf = info[j];
@@ -74,50 +74,42 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT,
   const int64_t bbeg = (int64_t)blockIdx.y * KS_CTS_PER_CTA;
   const int64_t bend = min(B, bbeg + KS_CTS_PER_CTA);
 
+  // mask accumulator in shared memory as [E/4][NT] 16-byte chunks: thread
+  // tid's chunk q sits at q * NT + tid, so a quarter-warp's 128-bit accesses
+  // cover 128 consecutive bytes (conflict-free)
+  uint4* acc1v = reinterpret_cast<uint4*>(acc1s);
+  const Mod32M mm{inf.p, 2 * inf.p, inf.pinv};
   for (int64_t b = bbeg; b < bend; ++b) {
     const uint32_t* dig = digits + b * dig_stride;
     uint32_t acc0[E], x[E];
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      acc0[e] = 0u;
-      acc1s[e * NT + tid] = 0u;
-    }
+    for (int e = 0; e < E; ++e) acc0[e] = 0u;
+#pragma unroll
+    for (int q = 0; q < E / 4; ++q) acc1v[q * NT + tid] = make_uint4(0u, 0u, 0u, 0u);
 
     for (int i = 0; i < k; ++i) {
       const uint32_t* src = dig + (size_t)i * N;
 #pragma unroll
       for (int e = 0; e < E; ++e) x[e] = ld_stream(src + tid + e * NT);
       cta_fwd<LOGN, LOGE, Mod32>(md, x, sm, tws, twg);
-      const size_t koff = ((size_t)j * k + i) * N;
-      if constexpr ((1 << R) >= 4) {
+      const size_t koff = ((size_t)j * k + i) * N + row_index<LOGN, LOGE>(tid, 0);
+      const uint4* kb = reinterpret_cast<const uint4*>(kbody + koff);
+      const uint4* km = reinterpret_cast<const uint4*>(kmask + koff);
 #pragma unroll
-        for (int bb = 0; bb < G_::BLK; ++bb) {
-          const size_t o = koff + row_index<LOGN, LOGE>(tid, bb << R);
-          const uint4* kb = reinterpret_cast<const uint4*>(kbody + o);
-          const uint4* km = reinterpret_cast<const uint4*>(kmask + o);
+      for (int q = 0; q < E / 4; ++q) {
+        const uint4 wb = ld_stream_v4(kb + q);
+        const uint4 wm = ld_stream_v4(km + q);
+        uint4 a1 = acc1v[q * NT + tid];
+        const uint32_t kbv[4] = {wb.x, wb.y, wb.z, wb.w};
+        const uint32_t kmv[4] = {wm.x, wm.y, wm.z, wm.w};
+        uint32_t a1v[4] = {a1.x, a1.y, a1.z, a1.w};
 #pragma unroll
-          for (int v = 0; v < (1 << R) / 4; ++v) {
-            const uint4 wb = ld_stream_v4(kb + v);
-            const uint4 wm = ld_stream_v4(km + v);
-            const uint32_t kbv[4] = {wb.x, wb.y, wb.z, wb.w};
-            const uint32_t kmv[4] = {wm.x, wm.y, wm.z, wm.w};
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int e = bb * (1 << R) + v * 4 + q;
-              acc0[e] = md.sub2p(acc0[e] + mont_mul_lazy(x[e], kbv[q], inf.p, inf.pinv_neg));
-              uint32_t& a1 = acc1s[e * NT + tid];
-              a1 = md.sub2p(a1 + mont_mul_lazy(x[e], kmv[q], inf.p, inf.pinv_neg));
-            }
-          }
+        for (int r = 0; r < 4; ++r) {
+          const int e = q * 4 + r;
+          acc0[e] = md.sub2p(acc0[e] + mm.mul(x[e], kbv[r]));
+          a1v[r] = md.sub2p(a1v[r] + mm.mul(x[e], kmv[r]));
         }
-      } else {
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const size_t o = koff + row_index<LOGN, LOGE>(tid, e);
-          acc0[e] = md.sub2p(acc0[e] + mont_mul_lazy(x[e], __ldg(kbody + o), inf.p, inf.pinv_neg));
-          uint32_t& a1 = acc1s[e * NT + tid];
-          a1 = md.sub2p(a1 + mont_mul_lazy(x[e], __ldg(kmask + o), inf.p, inf.pinv_neg));
-        }
+        acc1v[q * NT + tid] = make_uint4(a1v[0], a1v[1], a1v[2], a1v[3]);
       }
     }
 
@@ -126,7 +118,13 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT,
     for (int part = 0; part < 2; ++part) {
       if (part == 1) {
 #pragma unroll
-        for (int e = 0; e < E; ++e) acc0[e] = acc1s[e * NT + tid];
+        for (int q = 0; q < E / 4; ++q) {
+          const uint4 a1 = acc1v[q * NT + tid];
+          acc0[4 * q] = a1.x;
+          acc0[4 * q + 1] = a1.y;
+          acc0[4 * q + 2] = a1.z;
+          acc0[4 * q + 3] = a1.w;
+        }
       }
       cta_inv<LOGN, LOGE, Mod32>(md, acc0, sm, itw, inf.ninv, inf.wn);
       uint32_t* o = (part ? out1 : out0) + s * out_stride + (size_t)j * N;
@@ -155,7 +153,7 @@ static int run_ks(hefv_ctx* c, const uint32_t* kb, const uint32_t* km, const uin
   typedef Geo<LOGN, LE> G_;
   auto kern = k_keyswitch<LOGN, LE>;
   const size_t smem = (size_t)(1 << (LOGN - G_::RLAST)) * sizeof(uint2) +
-                      ((size_t)G_::N + (size_t)spad_size(G_::N)) * 4;
+                      ((size_t)G_::N + (size_t)((spad_size(G_::N) + 3) & ~3)) * 4;
   if (smem > 48 * 1024) {
     HEFV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   }
