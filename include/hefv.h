@@ -188,6 +188,19 @@ int hefv_accumulate_rows(hefv_ctx* ctx, const uint32_t* rows, const int32_t* seg
 int hefv_add_part0(hefv_ctx* ctx, uint32_t* rows, int64_t row_stride, const int32_t* slot,
                    const uint32_t* add, int64_t P, void* stream);
 
+/* ---- 64-bit RNS key switch (config-4 microbench; _keyswitch_apply,
+ * fv.py:205-217, for 50-62-bit primes) --------------------------------------
+ * Context: the L 64-bit primes of the context.  kbody/kmask: (L, L, N) =
+ * [target j][digit i], device NTT order, Montgomery form (x * 2^64 mod p_j);
+ * digits: (B, L, N) coefficient limbs; out: (B, 2, L, N) coefficient domain;
+ * scratch: B * L * L * N words. */
+int hefv_keyswitch64(hefv_ctx* ctx, const uint64_t* kbody, const uint64_t* kmask,
+                     const uint64_t* digits, uint64_t* out, uint64_t* scratch, int64_t B,
+                     void* stream);
+/* (rows, L, N) -> Montgomery form x * 2^64 mod p_j. */
+int hefv_to_montgomery64(hefv_ctx* ctx, const uint64_t* in, uint64_t* out, int64_t rows,
+                         void* stream);
+
 /* ---- measurement ---------------------------------------------------------
  * Integer-pipe throughput probe (roofline denominator; not a reference
  * function): kind 0 IMAD, 1 IMAD.HI, 2 IMAD.WIDE, 3 IADD3, 4 Shoup butterfly;

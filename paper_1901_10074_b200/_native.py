@@ -48,6 +48,8 @@ _SIGS = {
     "hefv_accumulate_rows": [_P, _P, _P, _P, _P, _I32, _I32, _P],
     "hefv_add_part0": [_P, _P, _I64, _P, _P, _I64, _P],
     "hefv_probe_int": [_I32, _I32, _I32, _P, _P],
+    "hefv_keyswitch64": [_P, _P, _P, _P, _P, _P, _I64, _P],
+    "hefv_to_montgomery64": [_P, _P, _P, _I64, _P],
 }
 
 EXPORTED = tuple(["hefv_last_error", "hefv_ctx_destroy", "hefv_launch_count"] + list(_SIGS))

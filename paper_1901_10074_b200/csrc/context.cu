@@ -175,6 +175,13 @@ int hefv_ctx_create(hefv_ctx** out, uint32_t log_n, int32_t n32, const uint32_t*
     const uint64_t wn = mulmod(v[1], ninv, p);
     inf.wn.x = wn;
     inf.wn.y = (uint64_t)(((u128)wn << 64) / p);
+    uint64_t pinv = 1;  // Newton: p * pinv == 1 mod 2^64
+    for (int it = 0; it < 6; ++it) pinv *= 2ull - p * pinv;
+    inf.pinv_neg = 0ull - pinv;
+    {
+      const u128 r = ((u128)1 << 64) % p;  // 2^64 mod p
+      inf.r2 = (uint64_t)(r * r % p);
+    }
     c->info64.push_back(inf);
   }
   // ---- upload

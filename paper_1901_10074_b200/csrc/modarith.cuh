@@ -153,6 +153,17 @@ struct Prime64Info {
   uint64_t p;
   ulonglong2 ninv;
   ulonglong2 wn;
+  uint64_t pinv_neg;  // -p^{-1} mod 2^64 (Montgomery)
+  uint64_t r2;        // 2^128 mod p
 };
+
+// 64-bit Montgomery REDC of a*b (a < 2^64, b < p < 2^62): a*b*2^-64 mod p in [0, 2p).
+__device__ __forceinline__ uint64_t mont_mul64_lazy(uint64_t a, uint64_t b, uint64_t p,
+                                                    uint64_t pinv_neg) {
+  const uint64_t lo = a * b;
+  const uint64_t hi = __umul64hi(a, b);
+  const uint64_t m = lo * pinv_neg;
+  return hi + __umul64hi(m, p) + (lo != 0ull);
+}
 
 }  // namespace hefv
