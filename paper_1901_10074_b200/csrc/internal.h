@@ -46,6 +46,7 @@ struct hefv_ctx {
   int q_shift = 0;     // normalisation shift of q for long division
   uint32_t* d_delta = nullptr;   // Delta mod q_j (k)
   uint32_t* d_tmod = nullptr;    // t mod q_j (k)
+  bool ks_tmem = true;           // key switch: TMEM + bulk-copy variant when available
 };
 
 namespace hefv {

@@ -210,10 +210,18 @@ __device__ __forceinline__ void group_sync(int tid, const int GL) {
 // spad_size(N) words.  The exchange after full pass p only involves the
 // 2^(LOGN - (p+1) LOGE) threads that share a pass-p region, so only the first
 // exchange is CTA-wide; later ones use group / warp barriers.
-template <int LOGN, int LOGE, class M>
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+// `hook` runs right after the first CTA-wide barrier of the transform, i.e.
+// once every thread has consumed its input registers' source (used to
+// recycle an input staging buffer).
+template <int LOGN, int LOGE, class M, class Hook = NoHook>
 __device__ __forceinline__ void cta_fwd(const M& md, typename M::T* x, typename M::T* sm,
                                         const typename M::Tw* __restrict__ tw,
-                                        const typename M::Tw* __restrict__ tw_last = nullptr) {
+                                        const typename M::Tw* __restrict__ tw_last = nullptr,
+                                        const Hook& hook = Hook()) {
   typedef Geo<LOGN, LOGE> G_;
   constexpr int LOG_NT = LOGN - LOGE;
   const int tid = threadIdx.x;
@@ -224,6 +232,7 @@ __device__ __forceinline__ void cta_fwd(const M& md, typename M::T* x, typename 
     // be read by the previous transform), group-wide afterwards
     if (pass == 0) {
       __syncthreads();
+      hook();
     } else {
       group_sync<LOG_NT>(tid, LOGN - (pass + 1) * LOGE);
     }

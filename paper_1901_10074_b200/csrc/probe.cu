@@ -7,11 +7,40 @@
 //   kind 2: IMAD.WIDE (32x32 -> 64-bit product)
 //   kind 3: IADD3     (ALU pipe reference)
 //   kind 4: one lazy Shoup Cooley-Tukey butterfly (counted as 1 op)
+//   kind 5: one lazy 64-bit Shoup butterfly (p < 2^62; counted as 1 op)
 // Each thread runs 8 independent chains so the pipes, not latency, bound it.
 #include "../../include/hefv.h"
 #include "internal.h"
 
 namespace hefv {
+
+__global__ void __launch_bounds__(256) k_probe64(uint32_t* out, int iters, uint32_t seed) {
+  uint64_t a[8], b[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    a[i] = (uint64_t)(seed * (threadIdx.x + 1) + i) * 0x9e3779b97f4a7c15ull >> 3;
+    b[i] = ((uint64_t)(seed ^ (blockIdx.x * 131u + i)) * 0xbf58476d1ce4e5b9ull) >> 3;
+  }
+  const uint64_t p = 4611686018427322369ull, p2 = 2 * p;  // 2^62 - 2^16 + 1 (prime)
+  const uint64_t w = 1234567890123456789ull % p, wsh = (uint64_t)(((unsigned __int128)w << 64) / p);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint64_t x = a[i] >= p2 ? a[i] - p2 : a[i];
+        const uint64_t q = __umul64hi(b[i], wsh);
+        const uint64_t t = b[i] * w - q * p;
+        a[i] = x + t;
+        b[i] = x - t + p2;
+      }
+    }
+  }
+  uint64_t s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s ^= a[i] ^ b[i];
+  if (s == 0x12345678ull) out[0] = (uint32_t)s;
+}
 
 template <int KIND>
 __global__ void __launch_bounds__(256) k_probe(uint32_t* out, int iters, uint32_t seed) {
@@ -77,6 +106,9 @@ extern "C" int hefv_probe_int(int32_t kind, int32_t blocks, int32_t iters, uint3
       break;
     case 4:
       k_probe<4><<<blocks, 256, 0, st>>>(out, iters, 7u);
+      break;
+    case 5:
+      k_probe64<<<blocks, 256, 0, st>>>(out, iters, 7u);
       break;
     default:
       return fail("hefv_probe_int: unknown kind");
