@@ -103,7 +103,8 @@ int hefv_ctx_create(hefv_ctx** out, uint32_t log_n, int32_t n32, const uint32_t*
   if (log_n < 1 || log_n > 16) return fail("hefv_ctx_create: log_n must be in [1, 16]");
   if (n32 < 0 || n64 < 0 || n32 + n64 == 0) return fail("hefv_ctx_create: empty prime set");
   hefv_ctx* c = new hefv_ctx();
-  if (const char* v = std::getenv("HEFV_KS_TMEM")) c->ks_tmem = std::atoi(v) != 0;
+  if (const char* v = std::getenv("HEFV_KS_TMEM")) c->ks_tmem = std::atoi(v);
+  if (const char* v = std::getenv("HEFV_KS_E32")) c->ks_e32 = std::atoi(v);
   c->log_n = (int)log_n;
   c->n = 1 << log_n;
   const int n = c->n;

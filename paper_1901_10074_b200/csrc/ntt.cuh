@@ -104,7 +104,9 @@ __device__ __forceinline__ void fwd_full_pass(const M& md, typename M::T* x, int
 
 template <int LOGN, int LOGE, class M>
 __device__ __forceinline__ void fwd_last_pass(const M& md, typename M::T* x, int tid,
-                                              const typename M::Tw* __restrict__ tw) {
+                                              const typename M::Tw* __restrict__ tw,
+                                              const typename M::Tw* __restrict__ tw_hi = nullptr,
+                                              int split_log = 31) {
   typedef Geo<LOGN, LOGE> G_;
   constexpr int R = G_::RLAST;
   constexpr int s0 = LOGN - R;
@@ -115,7 +117,10 @@ __device__ __forceinline__ void fwd_last_pass(const M& md, typename M::T* x, int
   for (int l = 0; l < R; ++l) {
     const int half = (1 << R) >> (l + 1);
     typename M::Tw w[BLK << (R - 1)];
-    load_tw_run<typename M::Tw, (BLK << (R - 1))>(tw + (1 << (s0 + l)) + ((tid * BLK) << l), w,
+    // stages whose table slice lies below 2^split_log read `tw` (e.g. a shared
+    // copy), the others `tw_hi` (global, through L1)
+    const typename M::Tw* src = (tw_hi == nullptr || s0 + l + 1 <= split_log) ? tw : tw_hi;
+    load_tw_run<typename M::Tw, (BLK << (R - 1))>(src + (1 << (s0 + l)) + ((tid * BLK) << l), w,
                                                   BLK << l);
 #pragma unroll
     for (int b = 0; b < BLK; ++b) {
@@ -221,7 +226,7 @@ template <int LOGN, int LOGE, class M, class Hook = NoHook>
 __device__ __forceinline__ void cta_fwd(const M& md, typename M::T* x, typename M::T* sm,
                                         const typename M::Tw* __restrict__ tw,
                                         const typename M::Tw* __restrict__ tw_last = nullptr,
-                                        const Hook& hook = Hook()) {
+                                        const Hook& hook = Hook(), int split_log = 0) {
   typedef Geo<LOGN, LOGE> G_;
   constexpr int LOG_NT = LOGN - LOGE;
   const int tid = threadIdx.x;
@@ -248,7 +253,11 @@ __device__ __forceinline__ void cta_fwd(const M& md, typename M::T* x, typename 
       for (int e = 0; e < G_::E; ++e) x[e] = sm[xaddr_row<LOGN, LOGE>(tid, e, K, S)];
     }
   }
-  fwd_last_pass<LOGN, LOGE, M>(md, x, tid, tw_last ? tw_last : tw);
+  // last pass: stages with table entries below 2^split_log from `tw`, the rest from tw_last
+  if (tw_last == nullptr)
+    fwd_last_pass<LOGN, LOGE, M>(md, x, tid, tw);
+  else
+    fwd_last_pass<LOGN, LOGE, M>(md, x, tid, tw, tw_last, split_log);
 }
 
 // ---- inverse (Gentleman-Sande, bit-reversed -> natural) -------------------
