@@ -228,10 +228,10 @@ def run_ours(args, rank, local_rank, world):
         avg_launch_ms = ks_ms / max(1, ks_launches)
         cts_per_launch = ks_cts / max(1, ks_launches)
         achieved = work["modmuls"] * cts_per_launch / (avg_launch_ms * 1e-3) / 1e12
-        traffic = _ncu_traffic()
+        traffic = _ncu_traffic(ks_cts / max(1, ks_launches))
         counts = workload_op_counts(cfg)
         roofline = {
-            "kernel": "k_keyswitch<14,5> (fused digit NTT -> MAC -> iNTT)",
+            "kernel": "k_keyswitch<14,4> (fused digit NTT -> MAC -> iNTT)",
             "bound": "int-pipe (IMAD)", "unit": "Tmodmul/s",
             "achieved": round(achieved, 3), "peak": round(peak["shoup_butterfly"], 3),
             "frac": round(achieved / peak["shoup_butterfly"], 4),
@@ -298,15 +298,20 @@ def _hbm_peak():
         return 6650.0
 
 
-def _ncu_traffic():
-    """dram bytes per k_keyswitch launch from the committed ncu capture, or None."""
+def _ncu_traffic(cts_per_launch=None):
+    """dram bytes (read + write) per k_keyswitch launch from the committed ncu
+    capture (profiles/ks_traffic.json), scaled to this run's average launch."""
     p = ROOT / "profiles" / "ks_traffic.json"
-    if p.exists():
-        try:
-            return json.loads(p.read_text()).get("dram_bytes_per_launch")
-        except Exception:
-            return None
-    return None
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+    except Exception:
+        return None
+    per_ct = d.get("dram_bytes_per_ct")
+    if per_ct is None or cts_per_launch is None:
+        return d.get("dram_bytes_per_launch")
+    return int(per_ct * cts_per_launch)
 
 
 def _cpu_baseline_single(params, counts) -> dict:

@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT,
     for (int i = tid; i < NTW / 2; i += NT) dst[i] = __ldg(src + i);
   }
   __syncthreads();
+  const uint64_t kpol = l2_policy_evict_last();
   const uint2* itw = itw_all + (size_t)j * N;
   const int64_t bbeg = (int64_t)blockIdx.y * KS_CTS_PER_CTA;
   const int64_t bend = min(B, bbeg + KS_CTS_PER_CTA);
@@ -101,8 +102,8 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT,
       const uint4* km = reinterpret_cast<const uint4*>(kmask + koff);
 #pragma unroll
       for (int q = 0; q < E / 4; ++q) {
-        const uint4 wb = ld_stream_v4(kb + q);
-        const uint4 wm = ld_stream_v4(km + q);
+        const uint4 wb = ld_key_v4(kb + q, kpol);
+        const uint4 wm = ld_key_v4(km + q, kpol);
         uint4 a1 = acc1v[q * NT + tid];
         const uint32_t kbv[4] = {wb.x, wb.y, wb.z, wb.w};
         const uint32_t kmv[4] = {wm.x, wm.y, wm.z, wm.w};
