@@ -89,14 +89,15 @@ __device__ __forceinline__ void fwd_full_pass(const M& md, typename M::T* x, int
 #pragma unroll
   for (int l = 0; l < LOGE; ++l) {
     const int half = G_::E >> (l + 1);
-    const typename M::Tw* twb = tw + (1 << (s0 + l)) + (G << l);
+    // the 2^l twiddles of this stage are contiguous: 16-byte loads
+    typename M::Tw w[1 << (LOGE - 1)];
+    load_tw_run<typename M::Tw, (1 << (LOGE - 1))>(tw + (1 << (s0 + l)) + (G << l), w, 1 << l);
 #pragma unroll
     for (int u = 0; u < (1 << l); ++u) {
-      const typename M::Tw w = twb[u];
 #pragma unroll
       for (int e0 = 0; e0 < half; ++e0) {
         const int e = u * 2 * half + e0;
-        md.ct(x[e], x[e + half], w);
+        md.ct(x[e], x[e + half], w[u]);
       }
     }
   }
