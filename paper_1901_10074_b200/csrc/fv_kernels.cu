@@ -591,7 +591,7 @@ static int run_rows_mac(hefv_ctx* c, const uint32_t* x, const uint32_t* m, const
 // Galois automorphism x -> x^g on coefficients (fv.py:157-173):
 // out[m] = in[j1] if j1 = m g^-1 mod 2N < N, else -in[j1 - N].
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024)
+__global__ void __launch_bounds__(512)
     k_automorph(const uint32_t* __restrict__ in, int64_t in_stride, const int32_t* __restrict__ slot,
                 uint32_t* __restrict__ out, int nparts, int k, int log_n, uint32_t ginv,
                 const Prime32Info* __restrict__ info) {
@@ -605,19 +605,25 @@ __global__ void __launch_bounds__(1024)
   const uint32_t* src = in + src_ct * in_stride + (size_t)row * n;
   uint32_t* dst = out + (b * nparts * k + row) * (size_t)n;
   const uint32_t p = info[j].p;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) sm[i] = src[i];
+  // 16-byte coalesced staging of the source row
+  for (int i = threadIdx.x; i < n / 4; i += blockDim.x)
+    reinterpret_cast<uint4*>(sm)[i] = ld_stream_v4(reinterpret_cast<const uint4*>(src) + i);
   __syncthreads();
   const uint32_t mask = 2u * n - 1u;
-  for (int m = threadIdx.x; m < n; m += blockDim.x) {
-    const uint32_t j1 = ((uint32_t)m * ginv) & mask;
-    uint32_t v;
-    if (j1 < (uint32_t)n) {
-      v = sm[j1];
-    } else {
-      const uint32_t w = sm[j1 - n];
-      v = w ? p - w : 0u;
+  for (int q = threadIdx.x; q < n / 4; q += blockDim.x) {
+    uint32_t v[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const uint32_t m = 4u * q + r;
+      const uint32_t j1 = (m * ginv) & mask;
+      if (j1 < (uint32_t)n) {
+        v[r] = sm[j1];
+      } else {
+        const uint32_t w = sm[j1 - n];
+        v[r] = w ? p - w : 0u;
+      }
     }
-    dst[m] = v;
+    reinterpret_cast<uint4*>(dst)[q] = make_uint4(v[0], v[1], v[2], v[3]);
   }
 }
 
@@ -851,7 +857,8 @@ int hefv_automorph(hefv_ctx* c, const uint32_t* in, int64_t in_stride, const int
   uint32_t g = galois_elt % two_n, inv = 1;
   for (int it = 0; it < 6; ++it) inv *= 2u - g * inv;
   inv &= two_n - 1u;
-  const int threads = c->n >= 1024 ? 1024 : c->n;
+  if (c->n < 16) return fail("hefv_automorph: N must be >= 16");
+  const int threads = c->n / 4 >= 512 ? 512 : c->n / 4;
   const size_t smem = (size_t)c->n * 4;
   if (smem > 48 * 1024) {
     HEFV_CUDA(cudaFuncSetAttribute(k_automorph, cudaFuncAttributeMaxDynamicSharedMemorySize,

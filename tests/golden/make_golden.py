@@ -226,3 +226,31 @@ if __name__ == "__main__":
     if "--retina" in sys.argv:
         gen_retina()
     del R_engine
+
+
+def gen_config3_rows():
+    """Config 3 (retina with 24 q primes): keys, the 24 input encryptions and
+    a subset of conv1 rows (all in output ciphertext 0) -- reference run."""
+    p = profile("retina").replace(coeff_modulus_bits=720)
+    t0 = time.time()
+    be = R_fv.FvBackend(p, rng=np.random.default_rng(1234))
+    tk = time.time() - t0
+    rng = np.random.default_rng(3)
+    img = rng.integers(0, 256, (3, 256, 256), dtype=np.int64)
+    c1 = R_inf.ConvSpec(8, (5, 5), (2, 2), (3, 256, 256), rng.integers(-8, 9, (8, 3, 5, 5)),
+                        np.zeros(8, np.int64))
+    pv = R_inf.pack_image(be, img)
+    rows = R_inf.compile_conv(c1, pv.slots_used)
+    pick = [0, 1, 126, 4095]
+    t1 = time.time()
+    res = R_inf.layer_eval(be, [rows[i] for i in pick], pv)
+    out = {"key_seed": 1234, "data_seed": 3, "coeff_modulus_bits": 720,
+           "relin": key_digest(be.keys.relin), "enc": [digest(ct.parts) for ct in pv.cts],
+           "rows_pick": pick, "rows_out": [digest(ct.parts) for ct in res.cts],
+           "rows_cost": be.cost_report().as_dict(), "keygen_seconds": tk,
+           "rows_seconds": time.time() - t1}
+    dump("config3_rows.json", out)
+
+
+if __name__ == "__main__" and "--config3" in sys.argv:
+    gen_config3_rows()

@@ -124,3 +124,27 @@ def test_planner_equals_serial(s, skip):
     assert results[0][1] == results[1][1]
     assert results[0][2] == results[1][2]
     assert np.array_equal(results[0][3], results[1][3])
+
+
+@pytest.mark.slow
+def test_config3_rows_subset_matches_reference():
+    """Config 3 (24 q primes, three-channel input over 24 ciphertexts): keys,
+    encryptions and conv1 rows spanning several segments, bit-identical to the
+    reference's own run (tests/golden/config3_rows.json)."""
+    from paper_1901_10074_b200.fv import FvBackend
+
+    path = GOLD / "config3_rows.json"
+    if not path.exists():
+        pytest.skip("config3 golden not generated")
+    g = json.loads(path.read_text())
+    img, net = config_network(3)
+    be = FvBackend(config_params(3), rng=np.random.default_rng(g["key_seed"]))
+    from oracle.fv_oracle import limb_digest as ld
+
+    assert ld(list(be.keys.relin.body) + list(be.keys.relin.mask)) == g["relin"]
+    pv = I.pack_image(be, img)
+    assert [limb_digest(ct.parts) for ct in pv.cts] == g["enc"]
+    rows = I.compile_conv(net.layers[0], pv.slots_used)
+    res = I.layer_eval(be, [rows[i] for i in g["rows_pick"]], pv)
+    assert [limb_digest(ct.parts) for ct in res.cts] == g["rows_out"]
+    assert be.cost_report().as_dict() == g["rows_cost"]
