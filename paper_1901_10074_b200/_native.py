@@ -114,6 +114,17 @@ def to_device(arr):
     return torch.from_numpy(a).cuda()
 
 
+def to_device_async(arr):
+    """numpy -> CUDA tensor through pinned memory, asynchronous on the current
+    stream (the host keeps enqueueing while the GPU works)."""
+    import numpy as np
+    import torch
+
+    a = np.ascontiguousarray(arr)
+    TRAFFIC["h2d"] += a.nbytes
+    return torch.from_numpy(a).pin_memory().to("cuda", non_blocking=True)
+
+
 def to_host(t):
     """CUDA tensor -> numpy (counted as device-to-host traffic)."""
     TRAFFIC["d2h"] += t.numel() * t.element_size()

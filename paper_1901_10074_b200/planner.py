@@ -253,6 +253,35 @@ def planned_layer_eval(backend, rows, x, skip_zero_segments=True, scale_factor=1
     return PackedVector(R, s, out, scale=x.scale * scale_factor)
 
 
+def _sparse_plan(rows, order, s: int, t: int) -> dict:
+    """CSR of every (row, nonzero segment) plaintext, rows in `order`:
+    entries (slot, value mod t) grouped by plaintext, plaintexts grouped by
+    row (row_ptr), each tagged with its input segment.  Vectorised over the
+    whole layer -- identical to segment_dense (inference.py:68-73) per row."""
+    lens = np.fromiter((len(rows[i].positions) for i in order), dtype=np.int64, count=len(order))
+    if lens.sum() == 0:
+        z = np.zeros(1, dtype=np.int64)
+        return {"ptr": z, "slot": np.zeros(0, np.int32), "val": np.zeros(0, np.uint64),
+                "row_ptr": np.zeros(len(order) + 1, dtype=np.int64), "seg": np.zeros(0, np.int32)}
+    pos = np.concatenate([np.asarray(rows[i].positions, dtype=np.int64) for i in order])
+    raw = [np.asarray(rows[i].values) for i in order]
+    if any(v.dtype == object for v in raw):
+        val = np.array([int(w) % t for v in raw for w in v], dtype=np.uint64)
+    else:
+        val = np.mod(np.concatenate(raw).astype(np.int64), t).astype(np.uint64)
+    ridx = np.repeat(np.arange(len(order), dtype=np.int64), lens)
+    seg = pos // s
+    perm = np.lexsort((seg, ridx))  # stable: keeps position order inside a segment
+    pos, val, ridx, seg = pos[perm], val[perm], ridx[perm], seg[perm]
+    key = ridx * (int(seg.max()) + 1) + seg
+    starts = np.flatnonzero(np.concatenate(([True], key[1:] != key[:-1])))
+    ptr = np.concatenate((starts, [len(key)])).astype(np.int64)
+    g_row = ridx[starts]
+    row_ptr = np.searchsorted(g_row, np.arange(len(order) + 1), side="left").astype(np.int64)
+    return {"ptr": ptr, "slot": (pos % s).astype(np.int32), "val": val, "row_ptr": row_ptr,
+            "seg": seg[starts].astype(np.int32)}
+
+
 def _tile_rows(backend, n_plain_per_row: float) -> int:
     ctx = backend.ctx
     ct_bytes = 2 * ctx.k * ctx.n * 4
@@ -283,47 +312,34 @@ def _run_rows(backend, rows, x, seg_lists, active, m_arr, off_arr, bias_arr, out
     keys = backend.keys.galois
     slot_count = backend.params.slot_count
 
+    plan = _sparse_plan(rows, order, s, t)
+    up = nat.to_device_async
+
     for t0 in range(0, len(order), T):
         tile = order[t0:t0 + T]
         B = len(tile)
         # ---- 1. sparse plaintexts of every (row, nonzero segment) -------------
-        ptr = [0]
-        slot_idx = []
-        vals = []
-        row_ptr = [0]
-        plain_seg = []
-        for i in tile:
-            r = rows[i]
-            pos = np.asarray(r.positions, dtype=np.int64)
-            v = np.asarray(r.values)
-            segs_of = pos // s
-            for sg in seg_lists[i]:
-                sel = segs_of == sg
-                if not sel.any():
-                    continue  # all-zero segment: contributes the zero ciphertext
-                slot_idx.append(pos[sel] % s)
-                vs = v[sel]
-                if vs.dtype == object:
-                    vals.append(np.asarray([int(w) % t for w in vs], dtype=np.uint64))
-                else:
-                    vals.append(np.mod(vs.astype(np.int64), t).astype(np.uint64))
-                ptr.append(ptr[-1] + int(sel.sum()))
-                plain_seg.append(int(sg))
-            row_ptr.append(len(plain_seg))
-        P = len(plain_seg)
+        g_lo, g_hi = plan["row_ptr"][t0], plan["row_ptr"][t0 + B]
+        e_lo, e_hi = plan["ptr"][g_lo], plan["ptr"][g_hi]
+        P = int(g_hi - g_lo)
+        ptr = plan["ptr"][g_lo:g_hi + 1] - e_lo
+        slot_idx = [plan["slot"][e_lo:e_hi]]
+        vals = [plan["val"][e_lo:e_hi]]
+        row_ptr = plan["row_ptr"][t0:t0 + B + 1] - g_lo
+        plain_seg = plan["seg"][g_lo:g_hi]
         acc = torch.empty((B, 2, kq, n), dtype=torch.int32, device="cuda")
         if P:
-            d_ptr = nat.to_device(np.asarray(ptr, dtype=np.int32))
-            d_idx = nat.to_device(np.concatenate(slot_idx).astype(np.int32))
-            d_val = nat.to_device(np.concatenate(vals).view(np.int64))
+            d_ptr = up(np.asarray(ptr, dtype=np.int32))
+            d_idx = up(np.concatenate(slot_idx).astype(np.int32))
+            d_val = up(np.concatenate(vals).view(np.int64))
             polys = torch.empty((P, n), dtype=torch.int64, device="cuda")
             ctx.call("hefv_encode_sparse", d_ptr.data_ptr(), d_idx.data_ptr(), d_val.data_ptr(),
                      polys.data_ptr(), P, st)
             m_ntt = torch.empty((P, kq, n), dtype=torch.int32, device="cuda")
             ctx.call("hefv_plain_to_rns", polys.data_ptr(), m_ntt.data_ptr(), P, 1, 1, 0, st)
             del polys
-            d_rp = nat.to_device(np.asarray(row_ptr, dtype=np.int32))
-            d_ps = nat.to_device(np.asarray(plain_seg, dtype=np.int32))
+            d_rp = up(np.asarray(row_ptr, dtype=np.int32))
+            d_ps = up(np.asarray(plain_seg, dtype=np.int32))
             ctx.call("hefv_rows_mac", x_ntt.data_ptr(), m_ntt.data_ptr(), d_rp.data_ptr(),
                      d_ps.data_ptr(), acc.data_ptr(), B, st)
             del m_ntt
@@ -349,13 +365,13 @@ def _run_rows(backend, rows, x, seg_lists, active, m_arr, off_arr, bias_arr, out
             d_ptr = torch.arange(nb + 1, dtype=torch.int32, device="cuda")
             d_idx = torch.zeros(nb, dtype=torch.int32, device="cuda")
             bv = np.array([bias_arr[tile[bi]] % t for bi in bias_rows], dtype=np.uint64)
-            d_val = nat.to_device(bv.view(np.int64))
+            d_val = up(bv.view(np.int64))
             polys = torch.empty((nb, n), dtype=torch.int64, device="cuda")
             ctx.call("hefv_encode_sparse", d_ptr.data_ptr(), d_idx.data_ptr(), d_val.data_ptr(),
                      polys.data_ptr(), nb, st)
             dm = torch.empty((nb, kq, n), dtype=torch.int32, device="cuda")
             ctx.call("hefv_plain_to_rns", polys.data_ptr(), dm.data_ptr(), nb, 0, 0, 0, st)
-            d_slot = nat.to_device(np.asarray(bias_rows, dtype=np.int32))
+            d_slot = up(np.asarray(bias_rows, dtype=np.int32))
             ctx.call("hefv_add_part0", a0, ct_words, d_slot.data_ptr(), dm.data_ptr(), nb, st)
         ctx.call("hefv_mul_plain", a0, e0.data_ptr(), a0, B, 2, 1, st)
         # ---- 5. placement rotations by -off ------------------------------------------
@@ -370,7 +386,7 @@ def _run_rows(backend, rows, x, seg_lists, active, m_arr, off_arr, bias_arr, out
         # custom (non power-of-two) keys are single hops; power-of-two hops ascend
         for h in sorted(hop_groups, key=lambda v: (v & (v - 1) == 0, v)):
             idx = hop_groups[h]
-            d_slot = nat.to_device(np.asarray(idx, dtype=np.int32))
+            d_slot = up(np.asarray(idx, dtype=np.int32))
             nb = len(idx)
             sub = scr[:nb]
             b0 = sub.data_ptr()
@@ -386,8 +402,8 @@ def _run_rows(backend, rows, x, seg_lists, active, m_arr, off_arr, bias_arr, out
         bounds = np.flatnonzero(np.diff(ms)) + 1
         seg = np.concatenate([[0], bounds, [B]]).astype(np.int32)
         seg_out = ms[seg[:-1]].astype(np.int32)
-        d_seg = nat.to_device(seg)
-        d_out = nat.to_device(seg_out)
+        d_seg = up(seg)
+        d_out = up(seg_out)
         ctx.call("hefv_accumulate_rows", a0, d_seg.data_ptr(), d_out.data_ptr(),
                  out_dev.data_ptr(), len(seg_out), 1, st)
         del acc
