@@ -46,6 +46,7 @@ struct hefv_ctx {
   int q_shift = 0;     // normalisation shift of q for long division
   uint32_t* d_delta = nullptr;   // Delta mod q_j (k)
   uint32_t* d_tmod = nullptr;    // t mod q_j (k)
+  int ks_prefetch = 0;  // key switch: bulk-copy prefetch of the next digit into the tile (measured slower)
   int ks_e32 = 0;   // key switch at N = 2^14: 32 words per thread (512 threads)
   int ks_tmem = 0;  // key switch: 0 plain, 1 TMEM mask acc (E=16), 2 both accs in TMEM (E=32)
 };

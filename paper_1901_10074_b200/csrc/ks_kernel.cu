@@ -41,7 +41,11 @@ constexpr int KS_CTS_PER_CTA = 4;
 // [register e][thread] so every thread touches its own conflict-free words).
 // The body accumulator acc0 and the digit being transformed stay in
 // registers (2 E words per thread).
-template <int LOGN, int LOGE>
+// PREFETCH: the next digit limb is streamed into the exchange tile with a
+// bulk async copy (cp.async.bulk -> mbarrier) as soon as the current forward
+// transform has finished with the tile, so its L2/HBM latency hides behind
+// the last pass and the MAC.
+template <int LOGN, int LOGE, bool PREFETCH = false>
 __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT,
                                   Geo<LOGN, LOGE>::NT >= 512 ? 1 : 512 / Geo<LOGN, LOGE>::NT)
     k_keyswitch(const uint32_t* __restrict__ kbody, const uint32_t* __restrict__ kmask,
@@ -63,6 +67,7 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT,
   uint2* tws = reinterpret_cast<uint2*>(smraw);
   uint32_t* sm = reinterpret_cast<uint32_t*>(tws + NTW);  // exchange tile
   uint32_t* acc1s = sm + ((spad_size(N) + 3) & ~3);      // mask accumulator (16B aligned)
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(acc1s + N);
   const int j = blockIdx.x;
   const int tid = threadIdx.x;
   const Prime32Info inf = info[j];
@@ -84,6 +89,15 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT,
   // cover 128 consecutive bytes (conflict-free)
   uint4* acc1v = reinterpret_cast<uint4*>(acc1s);
   const Mod32M mm{inf.p, 2 * inf.p, inf.pinv};
+  uint32_t phase = 0;
+  if constexpr (PREFETCH) {
+    if (tid == 0) {
+      mbar_init(mbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) bulk_g2s(sm, digits + bbeg * dig_stride, N * 4, mbar);
+  }
   for (int64_t b = bbeg; b < bend; ++b) {
     const uint32_t* dig = digits + b * dig_stride;
     uint32_t acc0[E], x[E];
@@ -93,10 +107,25 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT,
     for (int q = 0; q < E / 4; ++q) acc1v[q * NT + tid] = make_uint4(0u, 0u, 0u, 0u);
 
     for (int i = 0; i < k; ++i) {
-      const uint32_t* src = dig + (size_t)i * N;
+      if constexpr (PREFETCH) {
+        mbar_wait(mbar, phase);
+        phase ^= 1u;
 #pragma unroll
-      for (int e = 0; e < E; ++e) x[e] = ld_stream(src + tid + e * NT);
+        for (int e = 0; e < E; ++e) x[e] = sm[tid + e * NT];
+      } else {
+        const uint32_t* src = dig + (size_t)i * N;
+#pragma unroll
+        for (int e = 0; e < E; ++e) x[e] = ld_stream(src + tid + e * NT);
+      }
       cta_fwd<LOGN, LOGE, Mod32>(md, x, sm, tws, twg, NoHook(), LOGN - R);
+      if constexpr (PREFETCH) {
+        if (i + 1 < k) {
+          // every thread is done with the tile: stream the next limb into it
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncthreads();
+          if (tid == 0) bulk_g2s(sm, dig + (size_t)(i + 1) * N, N * 4, mbar);
+        }
+      }
       const size_t koff = ((size_t)j * k + i) * N + row_index<LOGN, LOGE>(tid, 0);
       const uint4* kb = reinterpret_cast<const uint4*>(kbody + koff);
       const uint4* km = reinterpret_cast<const uint4*>(kmask + koff);
@@ -144,6 +173,13 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT,
         if (a) v = md.subp(v + a[idx]);
         if (c) v = md.subp(v + c[idx]);
         o[idx] = v;
+      }
+    }
+    if constexpr (PREFETCH) {
+      if (b + 1 < bend) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (tid == 0) bulk_g2s(sm, digits + (b + 1) * dig_stride, N * 4, mbar);
       }
     }
   }
@@ -371,9 +407,9 @@ static int run_ks_plain(hefv_ctx* c, const uint32_t* kb, const uint32_t* km, con
                         const uint32_t* a0, const uint32_t* a1, int64_t as, const uint32_t* b0,
                         const uint32_t* b1, int64_t bs, int64_t B, cudaStream_t st) {
   typedef Geo<LOGN, LE> G_;
-  auto kern = k_keyswitch<LOGN, LE>;
+  auto kern = (c->ks_prefetch && LOGN >= 10) ? k_keyswitch<LOGN, LE, true> : k_keyswitch<LOGN, LE, false>;
   const size_t smem = (size_t)(1 << (LOGN - G_::RLAST)) * sizeof(uint2) +
-                      ((size_t)G_::N + (size_t)((spad_size(G_::N) + 3) & ~3)) * 4;
+                      ((size_t)G_::N + (size_t)((spad_size(G_::N) + 3) & ~3)) * 4 + 16;
   if (smem > 48 * 1024) {
     HEFV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   }
