@@ -14,7 +14,8 @@ from pathlib import Path
 
 from .errors import NativeError
 
-_LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libhefv.so"
+_LIB_PATH = Path(os.environ.get("HEFV_LIB") or
+                 Path(__file__).resolve().parent / "_lib" / "libhefv.so")
 
 _P = C.c_void_p
 _I32 = C.c_int32

@@ -34,7 +34,10 @@ struct KsLoge {
 
 // Ciphertexts handled per CTA: the forward twiddle table of the CTA's prime
 // is staged in shared memory once and reused for CH * k digit transforms.
-constexpr int KS_CTS_PER_CTA = 4;
+#ifndef HEFV_KS_CTS
+#define HEFV_KS_CTS 4
+#endif
+constexpr int KS_CTS_PER_CTA = HEFV_KS_CTS;
 
 // Shared memory: Montgomery-form forward twiddles of prime j (N words), the
 // padded exchange tile, and the mask accumulator acc1 (N words, laid out

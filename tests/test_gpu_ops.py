@@ -297,3 +297,49 @@ def test_mul_plain_and_keyswitch_batch_stress(name):
     single = be.rotate(a, 1).device()
     for b in range(B):
         assert torch.equal(out[b], single)
+
+
+def test_custom_rotation_keys_single_hop():
+    """keygen(rotation_offsets=...) adds non-power-of-two Galois keys; such a
+    rotation is one hop (fv.py:422-425), bit-identical to the oracle."""
+    from paper_1901_10074_b200.fv import FvBackend, FvParams, keygen
+
+    p = profile("desk")
+    fp = FvParams.from_backend(p)
+    gk = keygen(fp, rotation_offsets={5, 100, -3}, rng=np.random.default_rng(8))
+    assert {5, 100, 2045} <= set(gk.galois)
+    gpu = FvBackend(p, keys=gk, rng=np.random.default_rng(9))
+    ok = O.keygen(O.OracleParams.from_backend(p), rotation_offsets={5, 100, -3},
+                  rng=np.random.default_rng(8))
+    orc = O.OracleFvBackend(p, keys=ok, rng=np.random.default_rng(9))
+    assert np.array_equal(gpu.keys.galois[100].body[1], orc.keys.galois[100].body[1])
+    v = np.random.default_rng(1).integers(0, p.plain_modulus, p.slot_count)
+    ga, oa = gpu.encrypt(v), orc.encrypt(v)
+    for off in (5, 100, -3, 7):
+        assert _digest(gpu.rotate(ga, off).parts) == _digest(orc.rotate(oa, off).parts), off
+    assert gpu.rotation_hops(5) == [5] and gpu.rotation_hops(7) == [1, 2, 4]
+
+
+def test_planner_with_custom_keys_and_empty_layer():
+    from paper_1901_10074_b200 import inference as I
+    from paper_1901_10074_b200.fv import FvBackend, FvParams, keygen
+
+    p = profile("desk")
+    s = p.slot_count
+    results = []
+    for planned in (True, False):
+        gk = keygen(FvParams.from_backend(p), rotation_offsets={s - 3, s - 10},
+                    rng=np.random.default_rng(3))
+        be = FvBackend(p, keys=gk, rng=np.random.default_rng(4))
+        x = I.pack_image(be, np.arange(300).reshape(1, 1, -1))
+        rows = [I.WeightRow(out_index=i, length=300, slots_used=s,
+                            positions=np.array([i, i + 1], dtype=np.int64),
+                            values=np.array([2, -1], dtype=np.int64)) for i in range(12)]
+        out = I.layer_eval(be, rows, x) if planned else I._serial_layer_eval(be, rows, x, True, 1)
+        empty = I.layer_eval(be, [], x) if planned else I._serial_layer_eval(be, [], x, True, 1)
+        results.append(([_digest(ct.parts) for ct in out.cts + empty.cts],
+                        be.cost_report().as_dict(), I.decrypt_logits(be, out)))
+    assert results[0][0] == results[1][0]
+    assert results[0][1] == results[1][1]
+    want = [2 * i - (i + 1) for i in range(12)]
+    assert [int(v) for v in results[0][2]] == want
