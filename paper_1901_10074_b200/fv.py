@@ -21,7 +21,7 @@ import numpy as np
 
 from . import _native as nat
 from .engine import SlotBackend
-from .errors import ParamMismatchError
+from .errors import FormatError, ParamMismatchError
 from .params import BackendParams
 from .ring import (
     WORD_BITS,
@@ -268,19 +268,34 @@ class SwitchKey:
         self.mask_dev = mask_dev
 
     def _host(self, dev):
+        """Device layout -> reference layout: undo Montgomery (x * 2^-32 mod p,
+        exact in u64 since x, 2^-32 mod p < 2^30) and the device NTT order."""
         ctx = self._ctx
-        torch = _torch()
-        # undo Montgomery form: x * 2^-32 == mont(x, 1) -- do it on the host exactly
-        host = nat.to_host(dev).astype(np.int64)
+        host = nat.to_host(dev).astype(np.uint64)
         out = []
         for j, p in enumerate(ctx.q_primes):
-            rinv = pow(1 << 32, -1, p)
-            plain = (host[j].astype(object) * rinv % p).astype(np.int64)
+            plain = (host[j] * np.uint64(pow(1 << 32, -1, p)) % np.uint64(p)).astype(np.int64)
             nat_order = np.empty_like(plain)
             nat_order[..., ctx.brev] = plain
             out.append(nat_order)
-        del torch
         return out
+
+    @classmethod
+    def from_host(cls, ctx: FvContext, body, mask) -> "SwitchKey":
+        """Upload a key in the reference's stored form (list over target prime
+        j of (k, N) natural-order NTT values, fv.py:67-72) into the device
+        layout used by the key-switch kernel."""
+
+        def dev(stacks):
+            if len(stacks) != ctx.k or any(np.shape(s) != (ctx.k, ctx.n) for s in stacks):
+                raise FormatError("switch key does not match the parameter set")
+            arr = np.empty((ctx.k, ctx.k, ctx.n), dtype=np.uint32)
+            for j, p in enumerate(ctx.q_primes):
+                x = ctx.natural_to_dev(np.asarray(stacks[j], dtype=np.int64)).astype(np.uint64)
+                arr[j] = ((x % np.uint64(p)) << np.uint64(32)) % np.uint64(p)
+            return nat.to_device(arr.view(np.int32))
+
+        return cls(ctx, dev(body), dev(mask))
 
     @property
     def body(self):
@@ -302,6 +317,28 @@ class KeySet:
     galois: dict
     s_ntt: object = None    # (k, N) canonical device order
     _cache: dict = field(default_factory=dict)
+
+    @classmethod
+    def from_host(cls, ctx: FvContext, secret, public, relin, galois) -> "KeySet":
+        """Key set from the reference's stored form (serialize.read_keyset):
+        secret (k, N) residues, public coefficient pair, and (body, mask)
+        lists per switch key."""
+        secret = np.asarray(secret, dtype=np.int64)
+        if secret.shape != (ctx.k, ctx.n):
+            raise FormatError("secret key does not match the parameter set")
+        p0 = ctx.q_primes[0]
+        small = np.where(secret[0] > p0 // 2, secret[0] - p0, secret[0])
+        if np.abs(small).max(initial=0) > 1 or not np.array_equal(ctx.to_rns(small), secret):
+            raise FormatError("secret key is not ternary")
+        s_ntt = ctx.small_to_ntt(small)[0]
+        pk = np.stack([np.asarray(x, dtype=np.int64) for x in public])
+        pk_ntt = ctx.ntt_q(ctx.upload_residues(pk))
+        keys = cls(context=ctx, secret_small=small.astype(np.int8), pk_ntt=pk_ntt,
+                   relin=SwitchKey.from_host(ctx, *relin),
+                   galois={int(off): SwitchKey.from_host(ctx, *bm) for off, bm in galois.items()},
+                   s_ntt=s_ntt)
+        keys._cache["public"] = (pk[0], pk[1])
+        return keys
 
     @property
     def secret(self) -> np.ndarray:

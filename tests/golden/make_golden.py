@@ -254,3 +254,42 @@ def gen_config3_rows():
 
 if __name__ == "__main__" and "--config3" in sys.argv:
     gen_config3_rows()
+
+
+def gen_serialize():
+    """Wire-format bytes written by the reference's own serialize module:
+    sha256 of a FV ciphertext record, an encrypted image (config 1 input), a
+    logits record, and each file of a desk key directory."""
+    import io
+    import tempfile
+
+    from hepack import serialize as R_ser
+
+    p = profile("desk")
+    be = R_fv.FvBackend(p, rng=np.random.default_rng(77))
+    rng = np.random.default_rng(5)
+    v = rng.integers(0, p.plain_modulus, p.slot_count)
+    ct = be.encrypt(v)
+    buf = io.BytesIO()
+    R_ser.write_ciphertext(buf, ct, p)
+    out = {"key_seed": 77, "data_seed": 5,
+           "ct_record": hashlib.sha256(buf.getvalue()).hexdigest(),
+           "ct_record_len": len(buf.getvalue())}
+    img, _ = net_for(1)
+    pv = R_inf.pack_image(be, img)
+    with tempfile.TemporaryDirectory() as d:
+        R_ser.write_encrypted_image(f"{d}/img.enc", pv, p)
+        out["image"] = hashlib.sha256(open(f"{d}/img.enc", "rb").read()).hexdigest()
+        slot_map = [(0, 0), (0, 1)]
+        R_ser.write_logits(f"{d}/logits.bin", [ct, pv.cts[0]], slot_map, p)
+        out["logits"] = hashlib.sha256(open(f"{d}/logits.bin", "rb").read()).hexdigest()
+        fp = R_fv.FvParams.from_backend(p)
+        R_ser.write_keyset(f"{d}/keys", be.keys, fp, p)
+        out["keyset"] = {name: hashlib.sha256(open(f"{d}/keys/{name}", "rb").read()).hexdigest()
+                         for name in ("params.json", "secret.bin", "public.bin", "relin.bin",
+                                      "galois.bin")}
+    dump("serialize.json", out)
+
+
+if __name__ == "__main__" and "--serialize" in sys.argv:
+    gen_serialize()
