@@ -139,6 +139,14 @@ int hefv_mul_plain(hefv_ctx* ctx, const uint32_t* ct, const uint32_t* m_ntt, uin
 int hefv_rows_mac(hefv_ctx* ctx, const uint32_t* x_ntt, const uint32_t* m_ntt,
                   const int32_t* row_ptr, const int32_t* plain_seg, uint32_t* out, int64_t R,
                   void* stream);
+/* The same MAC with a plaintext index per tap: row r sums, over taps t in
+ * [row_ptr[r], row_ptr[r+1]), m_ntt[tap_plain[t]] * x_ntt[tap_src[t]].  Used
+ * by the interleaved (per-pixel broadcast) layers, inference.py:406-428:
+ * every cmult by np.full(width, w) shares the plaintext of its weight value,
+ * and the row's cmult + add chain is one NTT-domain sum (linear, exact). */
+int hefv_rows_mac_indexed(hefv_ctx* ctx, const uint32_t* x_ntt, const uint32_t* m_ntt,
+                          const int32_t* row_ptr, const int32_t* tap_src,
+                          const int32_t* tap_plain, uint32_t* out, int64_t R, void* stream);
 
 /* ---- rotations (fv.py:157-173, fv.py:417-432) -----------------------------
  * Galois automorphism x -> x^g (g odd) of `nparts` parts of B ciphertexts:
@@ -176,6 +184,13 @@ int hefv_keygen_digit(hefv_ctx* ctx, const uint32_t* a_i, const int8_t* e_i, int
  * parts; scratch: at least 7 * a * N uint32 (aux stacks). */
 int hefv_mult_tensor(hefv_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out3,
                      uint32_t* scratch, void* stream);
+/* Batched tensor step of B products a[i] x b[i]: a[i] = a + i * a_stride,
+ * b[i] = b + i * b_stride (uint32 words), out3 (B, 3, k, N), scratch
+ * B * 7 * a * N words.  a == b with equal strides are squares (only the two
+ * parts of each operand are lifted). */
+int hefv_mult_tensor_many(hefv_ctx* ctx, const uint32_t* a, int64_t a_stride, const uint32_t* b,
+                          int64_t b_stride, uint32_t* out3, uint32_t* scratch, int64_t B,
+                          void* stream);
 
 /* ---- layer planner helpers ---------------------------------------------------
  * out[dst] (+)= sum of rows[r] for r in [seg[m], seg[m+1]) for m < M, with

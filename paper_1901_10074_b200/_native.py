@@ -46,8 +46,10 @@ _SIGS = {
     "hefv_keyswitch": [_P, _P, _P, _P, _I64, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _I64, _I64, _P],
     "hefv_keygen_digit": [_P, _P, _P, _I32, _P, _P, _P, _P, _P, _P],
     "hefv_mult_tensor": [_P, _P, _P, _P, _P, _P],
+    "hefv_mult_tensor_many": [_P, _P, _I64, _P, _I64, _P, _P, _I64, _P],
     "hefv_accumulate_rows": [_P, _P, _P, _P, _P, _I32, _I32, _P],
     "hefv_add_part0": [_P, _P, _I64, _P, _P, _I64, _P],
+    "hefv_rows_mac_indexed": [_P, _P, _P, _P, _P, _P, _P, _I64, _P],
     "hefv_probe_int": [_I32, _I32, _I32, _P, _P],
     "hefv_keyswitch64": [_P, _P, _P, _P, _P, _P, _I64, _P],
     "hefv_to_montgomery64": [_P, _P, _P, _I64, _P],

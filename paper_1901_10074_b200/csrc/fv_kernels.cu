@@ -542,8 +542,8 @@ template <int LOGN>
 __global__ void __launch_bounds__(Geo<LOGN, Loge32<LOGN>::v>::NT)
     k_rows_mac(const uint32_t* __restrict__ x_ntt, const uint32_t* __restrict__ m_ntt,
                const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ plain_seg,
-               uint32_t* __restrict__ out, int k, const uint2* __restrict__ itw_all,
-               const Prime32Info* __restrict__ info) {
+               const int32_t* __restrict__ plain_idx, uint32_t* __restrict__ out, int k,
+               const uint2* __restrict__ itw_all, const Prime32Info* __restrict__ info) {
   constexpr int LE = Loge32<LOGN>::v;
   typedef Geo<LOGN, LE> G_;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -562,7 +562,8 @@ __global__ void __launch_bounds__(Geo<LOGN, Loge32<LOGN>::v>::NT)
   for (int p = lo; p < hi; ++p) {
     const int seg = plain_seg[p];
     const uint32_t* xs = x_ntt + (((size_t)seg * 2 + part) * k + j) * N;
-    const uint32_t* ms = m_ntt + ((size_t)p * k + j) * N;
+    const size_t mi = plain_idx != nullptr ? (size_t)plain_idx[p] : (size_t)p;
+    const uint32_t* ms = m_ntt + (mi * k + j) * N;
 #pragma unroll
     for (int e = 0; e < G_::E; ++e)
       acc[e] = md.sub2p(acc[e] + mont_mul_lazy(ms[row_index<LOGN, LE>(tid, e)], xs[row_index<LOGN, LE>(tid, e)], inf.p, inf.pinv_neg));
@@ -575,14 +576,16 @@ __global__ void __launch_bounds__(Geo<LOGN, Loge32<LOGN>::v>::NT)
 
 template <int LOGN>
 static int run_rows_mac(hefv_ctx* c, const uint32_t* x, const uint32_t* m, const int32_t* rp,
-                        const int32_t* seg, uint32_t* out, int64_t R, cudaStream_t st) {
+                        const int32_t* seg, const int32_t* pidx, uint32_t* out, int64_t R,
+                        cudaStream_t st) {
   if (R <= 0) return 0;
   if (R > 65535) return fail("rows_mac: more than 65535 rows per call");
   typedef Geo<LOGN, Loge32<LOGN>::v> G_;
   auto kern = k_rows_mac<LOGN>;
   if (int r = set_smem(kern, smem32<LOGN>())) return r;
   dim3 grid(c->k, 2, (unsigned)R);
-  kern<<<grid, G_::NT, smem32<LOGN>(), st>>>(x, m, rp, seg, out, c->k, c->d_itw32, c->d_info32);
+  kern<<<grid, G_::NT, smem32<LOGN>(), st>>>(x, m, rp, seg, pidx, out, c->k, c->d_itw32,
+                                             c->d_info32);
   HEFV_LAUNCH_CHECK("k_rows_mac");
   return 0;
 }
@@ -842,7 +845,16 @@ int hefv_rows_mac(hefv_ctx* c, const uint32_t* x_ntt, const uint32_t* m_ntt,
                   const int32_t* row_ptr, const int32_t* plain_seg, uint32_t* out, int64_t R,
                   void* stream) {
   if (int r = need_fv(c, "hefv_rows_mac")) return r;
-  HEFV_DISPATCH_FV(c->log_n, run_rows_mac, c, x_ntt, m_ntt, row_ptr, plain_seg, out, R,
+  HEFV_DISPATCH_FV(c->log_n, run_rows_mac, c, x_ntt, m_ntt, row_ptr, plain_seg,
+                   (const int32_t*)nullptr, out, R, as_stream(stream));
+}
+
+int hefv_rows_mac_indexed(hefv_ctx* c, const uint32_t* x_ntt, const uint32_t* m_ntt,
+                          const int32_t* row_ptr, const int32_t* tap_src,
+                          const int32_t* tap_plain, uint32_t* out, int64_t R, void* stream) {
+  if (int r = need_fv(c, "hefv_rows_mac_indexed")) return r;
+  if (tap_plain == nullptr) return fail("hefv_rows_mac_indexed: tap_plain is NULL");
+  HEFV_DISPATCH_FV(c->log_n, run_rows_mac, c, x_ntt, m_ntt, row_ptr, tap_src, tap_plain, out, R,
                    as_stream(stream));
 }
 

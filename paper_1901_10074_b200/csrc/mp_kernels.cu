@@ -13,6 +13,7 @@
 // double precision from below and corrected by an exact comparison; the
 // division by q is Knuth's algorithm D.  No approximate (BEHZ/HPS) rounding
 // is used anywhere, so the result equals Python's big-integer arithmetic.
+#include <algorithm>
 #include <cmath>
 
 #include "../../include/hefv.h"
@@ -248,15 +249,19 @@ __global__ void __launch_bounds__(128)
 // ---- ct x ct: centred lift q -> aux --------------------------------------
 // in: nparts ciphertext parts, each (k, N); out: (nparts, a, N)
 __global__ void __launch_bounds__(128)
-    k_mult_lift(const uint32_t* __restrict__ p0, const uint32_t* __restrict__ p1,
-                const uint32_t* __restrict__ p2, const uint32_t* __restrict__ p3, int nparts,
-                uint32_t* __restrict__ out, MpConsts mc, const Prime32Info* __restrict__ info) {
+    k_mult_lift(const uint32_t* __restrict__ a, int64_t a_stride, const uint32_t* __restrict__ b,
+                int64_t b_stride, int nparts, uint32_t* __restrict__ out, MpConsts mc,
+                const Prime32Info* __restrict__ info) {
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = 1ll << mc.log_n;
   if (gid >= nparts * n) return;
+  const int64_t ct = blockIdx.y;
   const int part = (int)(gid >> mc.log_n);
   const int64_t i = gid & (n - 1);
-  const uint32_t* src = part == 0 ? p0 : part == 1 ? p1 : part == 2 ? p2 : p3;
+  const int64_t stack_q = (int64_t)mc.k * n;
+  const uint32_t* src = part < 2 ? a + ct * a_stride + part * stack_q
+                                 : b + ct * b_stride + (part - 2) * stack_q;
+  out += ct * nparts * (int64_t)mc.a * n;
   uint32_t x[MAXWQ + 1], mag[MAXWQ];
   mp_crt(src + i, (size_t)n, mc.k, 0, mc.qhat, mc.qhatinv, mc.q, mc.wq, info, x);
   const bool neg = mp_cmp(x, mc.qhalf, mc.wq) > 0;  // x > floor(q/2) -> x - q
@@ -279,6 +284,8 @@ __global__ void k_mult_tensor(const uint32_t* __restrict__ L, int same, uint32_t
                               MpConsts mc, const Prime32Info* __restrict__ info) {
   const int64_t n = 1ll << mc.log_n;
   const int64_t stack = (int64_t)mc.a * n;
+  L += (int64_t)blockIdx.y * (same ? 2 : 4) * stack;
+  T += (int64_t)blockIdx.y * 3 * stack;
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < stack;
        g += (int64_t)gridDim.x * blockDim.x) {
     const int ai = (int)(g >> mc.log_n);
@@ -301,6 +308,8 @@ __global__ void __launch_bounds__(64)
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = 1ll << mc.log_n;
   if (gid >= 3 * n) return;
+  T += (int64_t)blockIdx.y * 3 * mc.a * n;
+  out += (int64_t)blockIdx.y * 3 * mc.k * n;
   const int st = (int)(gid >> mc.log_n);
   const int64_t i = gid & (n - 1);
   uint32_t x[MAXWM + 1], z[MAXWM + 3], un[MAXWM + 4], qw[MAXWM + 3];
@@ -360,33 +369,44 @@ extern "C" int hefv_decrypt_round(hefv_ctx* c, const uint32_t* acc, uint64_t* ou
   return 0;
 }
 
-extern "C" int hefv_mult_tensor(hefv_ctx* c, const uint32_t* a, const uint32_t* b,
-                                uint32_t* out3, uint32_t* scratch, void* stream) {
+extern "C" int hefv_mult_tensor_many(hefv_ctx* c, const uint32_t* a, int64_t a_stride,
+                                     const uint32_t* b, int64_t b_stride, uint32_t* out3,
+                                     uint32_t* scratch, int64_t B, void* stream) {
   if (!c || !c->fv_ready) return fail("hefv_mult_tensor: context without FV setup");
   if (c->a < 1 || c->wm < 1) return fail("hefv_mult_tensor: no auxiliary basis configured");
+  if (B <= 0) return 0;
+  if (B > 65535) return fail("hefv_mult_tensor: batch > 65535");
   cudaStream_t st = as_stream(stream);
   const int64_t n = c->n;
-  const int64_t stack_q = (int64_t)c->k * n;
   const int64_t stack_a = (int64_t)c->a * n;
-  const bool same = (a == b);
+  const bool same = (a == b) && (a_stride == b_stride);
   const int nparts = same ? 2 : 4;
-  uint32_t* L = scratch;                  // (nparts, a, N)
-  uint32_t* T = scratch + 4 * stack_a;    // (3, a, N)
+  uint32_t* L = scratch;                      // (B, nparts, a, N)
+  uint32_t* T = scratch + B * 4 * stack_a;    // (B, 3, a, N)
   const MpConsts mc = mp_consts(c);
   {
     const int64_t tot = nparts * n;
-    k_mult_lift<<<(unsigned)((tot + 127) / 128), 128, 0, st>>>(
-        a, a + stack_q, same ? a : b, same ? a + stack_q : b + stack_q, nparts, L, mc, c->d_info32);
+    dim3 grid((unsigned)((tot + 127) / 128), (unsigned)B);
+    k_mult_lift<<<grid, 128, 0, st>>>(a, a_stride, b, b_stride, nparts, L, mc, c->d_info32);
     HEFV_LAUNCH_CHECK("k_mult_lift");
   }
-  if (int r = hefv_ntt_fwd32(c, L, L, nparts, c->a, c->k, 0, stream)) return r;
-  k_mult_tensor<<<148 * 8, 256, 0, st>>>(L, same ? 1 : 0, T, mc, c->d_info32);
-  HEFV_LAUNCH_CHECK("k_mult_tensor");
-  if (int r = hefv_ntt_inv32(c, T, T, 3, c->a, c->k, 0, stream)) return r;
+  if (int r = hefv_ntt_fwd32(c, L, L, nparts * B, c->a, c->k, 0, stream)) return r;
+  {
+    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(148 * 8 / B + 1, (stack_a + 255) / 256));
+    k_mult_tensor<<<dim3(gx, (unsigned)B), 256, 0, st>>>(L, same ? 1 : 0, T, mc, c->d_info32);
+    HEFV_LAUNCH_CHECK("k_mult_tensor");
+  }
+  if (int r = hefv_ntt_inv32(c, T, T, 3 * B, c->a, c->k, 0, stream)) return r;
   {
     const int64_t tot = 3 * n;
-    k_mult_scale<<<(unsigned)((tot + 63) / 64), 64, 0, st>>>(T, out3, mc, c->d_info32);
+    dim3 grid((unsigned)((tot + 63) / 64), (unsigned)B);
+    k_mult_scale<<<grid, 64, 0, st>>>(T, out3, mc, c->d_info32);
     HEFV_LAUNCH_CHECK("k_mult_scale");
   }
   return 0;
+}
+
+extern "C" int hefv_mult_tensor(hefv_ctx* c, const uint32_t* a, const uint32_t* b,
+                                uint32_t* out3, uint32_t* scratch, void* stream) {
+  return hefv_mult_tensor_many(c, a, 0, b, 0, out3, scratch, 1, stream);
 }

@@ -631,6 +631,34 @@ class FvBackend(SlotBackend):
                  scratch.data_ptr(), ctx.stream())
         return self._relinearize(out3, level)
 
+    def _square_many_dev(self, devs, chunk=512):
+        """Squares of B ciphertexts (device stacks), batched: one tensor launch
+        sequence and one relinearisation key switch per chunk; each result is
+        limb-identical to ``_mult(a, a)``.  Returns a list of (2, k, N)."""
+        from .planner import keyswitch_call
+
+        torch = _torch()
+        ctx = self.ctx
+        key = self.keys.relin
+        stack = ctx.k * ctx.n
+        res = []
+        for lo in range(0, len(devs), chunk):
+            part = devs[lo:lo + chunk]
+            B = len(part)
+            a = torch.stack([d[:2] for d in part]).contiguous()
+            out3 = ctx.empty(B, 3, ctx.k, ctx.n)
+            scratch = ctx.empty(B * 7 * ctx.a * ctx.n)
+            ctx.call("hefv_mult_tensor_many", a.data_ptr(), 2 * stack, a.data_ptr(), 2 * stack,
+                     out3.data_ptr(), scratch.data_ptr(), B, ctx.stream())
+            del scratch, a
+            out = ctx.empty(B, 2, ctx.k, ctx.n)
+            keyswitch_call(ctx, key.body_dev.data_ptr(), key.mask_dev.data_ptr(),
+                           out3[0, 2].data_ptr(), 3 * stack, out[0, 0].data_ptr(),
+                           out[0, 1].data_ptr(), 2 * stack, None, out3[0, 0].data_ptr(),
+                           out3[0, 1].data_ptr(), 3 * stack, None, None, 0, B)
+            res += [out[i] for i in range(B)]
+        return res
+
     def _relinearize(self, out3, level):
         from .planner import keyswitch_call
 

@@ -217,7 +217,7 @@ def gen_retina():
     dump("retina.json", out)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) == 1 or "--retina" in sys.argv:
     gen_ntt()
     gen_primes()
     gen_fv_tiny()
@@ -293,3 +293,33 @@ def gen_serialize():
 
 if __name__ == "__main__" and "--serialize" in sys.argv:
     gen_serialize()
+
+
+def interleaved_net(inf):
+    """Small interleaved-baseline net: conv with a bias, square, FC with an
+    all-zero row (bias-only -> encryption) and a negative bias."""
+    rng = np.random.default_rng(11)
+    img = rng.integers(0, 16, (1, 6, 6), dtype=np.int64)
+    conv = inf.ConvSpec(2, (3, 3), (2, 2), (1, 6, 6), rng.integers(-4, 5, (2, 1, 3, 3)),
+                        np.array([3, 0], dtype=np.int64))
+    w = rng.integers(-4, 5, (3, conv.out_len))
+    w[2] = 0
+    fc = inf.FcSpec(3, w, np.array([1, -2, 5], dtype=np.int64))
+    return img, inf.NetworkSpec([conv, inf.SquareSpec(), fc], (1, 6, 6))
+
+
+def gen_interleaved():
+    img, net = interleaved_net(R_inf)
+    be = R_fv.FvBackend(profile("desk"), rng=np.random.default_rng(1234))
+    px = R_inf.pack_image_interleaved(be, img)
+    enc = [digest(ct.parts) for ct in px]
+    out = R_inf.interleaved_infer(be, net, px)
+    logits = R_inf.decrypt_logits(be, out)
+    dump("interleaved.json", {"key_seed": 1234, "enc": enc, "out": [digest(ct.parts) for ct in out],
+                              "levels": [ct.level_used for ct in out],
+                              "logits": [int(x) for x in logits],
+                              "cost": be.cost_report().as_dict()})
+
+
+if __name__ == "__main__" and "--interleaved" in sys.argv:
+    gen_interleaved()
