@@ -323,3 +323,21 @@ def gen_interleaved():
 
 if __name__ == "__main__" and "--interleaved" in sys.argv:
     gen_interleaved()
+
+
+def gen_matrix():
+    from hepack import matrix as R_mx
+
+    sys.path.insert(0, str(HERE.parent.parent))
+    sys.path.insert(0, str(HERE.parent))
+    from goldens import matrix_suite
+
+    be = R_fv.FvBackend(profile("desk"), rng=np.random.default_rng(1234))
+    t0 = time.time()
+    out = matrix_suite(be, R_mx, np.random.default_rng(17))
+    out.update({"key_seed": 1234, "data_seed": 17, "seconds": time.time() - t0})
+    dump("matrix.json", out)
+
+
+if __name__ == "__main__" and "--matrix" in sys.argv:
+    gen_matrix()

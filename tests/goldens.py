@@ -36,3 +36,35 @@ def replay_ops(be, g):
     return out, ops
 
 
+def matrix_suite(be, mx, rng):
+    """The matrix-path op sequence replayed by tests/test_matrix.py (reference
+    matrix.py on the FV backend): the single-ciphertext and the re-chunked
+    multi-ciphertext products, a layout conversion, a kept-layout transpose
+    and a plaintext-matrix product."""
+    res = {}
+    a3 = mx.PlainMatrix(3, 3, rng.integers(-7, 8, (3, 3)))
+    b3 = mx.PlainMatrix(3, 3, rng.integers(-7, 8, (3, 3)))
+    c = mx.mat_mul(be, mx.pack_matrix(be, a3, mx.Layout.RCP), mx.pack_matrix(be, b3, mx.Layout.CCP))
+    res["mm3"] = [O.limb_digest(ct.parts) for ct in c.cts]
+    res["mm3_plain"] = mx.unpack_matrix(be, c).entries.tolist()
+    a5 = mx.PlainMatrix(5, 5, rng.integers(-7, 8, (5, 5)))
+    b5 = mx.PlainMatrix(5, 5, rng.integers(-7, 8, (5, 5)))
+    c = mx.mat_mul(be, mx.pack_matrix(be, a5, mx.Layout.RCP, slots_used=13),
+                   mx.pack_matrix(be, b5, mx.Layout.CCP, slots_used=13))
+    res["mm5s13"] = [O.limb_digest(ct.parts) for ct in c.cts]
+    res["mm5s13_slots"] = c.slots_used
+    res["mm5s13_plain"] = mx.unpack_matrix(be, c).entries.tolist()
+    m34 = mx.PlainMatrix(3, 4, rng.integers(-7, 8, (3, 4)))
+    e = mx.convert_layout(be, mx.pack_matrix(be, m34, mx.Layout.RCP), mx.Layout.CP)
+    res["conv_cp"] = [O.limb_digest(ct.parts) for ct in e.cts]
+    tk = mx.mat_transpose(be, mx.pack_matrix(be, m34, mx.Layout.RCP, slots_used=5),
+                          keep_layout=True)
+    res["transpose_keep"] = [O.limb_digest(ct.parts) for ct in tk.cts]
+    w = mx.PlainMatrix(3, 6, rng.integers(-7, 8, (3, 6)))
+    xv = rng.integers(-7, 8, 6)
+    y = mx.plain_mat_mul(be, w, mx.pack_matrix(be, mx.PlainMatrix(6, 1, xv.reshape(-1, 1)),
+                                               mx.Layout.RCP, slots_used=4))
+    res["pmm"] = [O.limb_digest(ct.parts) for ct in y.cts]
+    res["pmm_plain"] = mx.unpack_matrix(be, y).entries.tolist()
+    res["cost"] = be.cost_report().as_dict()
+    return res
