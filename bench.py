@@ -126,12 +126,24 @@ def _max_over_ranks(value, world, device="cuda"):
 
 
 def _ks_work(ctx) -> dict:
-    """Algorithmic work of one key switch of one ciphertext:
-    modmuls M = (k^2 + 2k) ((N/2) log2 N + N) + 2 k^2 N, bytes = 2 k^2 N w / B + 3 k N w."""
+    """Algorithmic work of one key switch of one ciphertext.
+
+    Reference formulation (fv.py:205-217): M = (k^2 + 2k)
+    ((N/2) log2 N + N) + 2 k^2 N modmuls.  The aux-basis key switch that runs
+    here (ks_aux.cu) computes the same limbs with 3k forward + 6k inverse
+    transforms of (N/2) log2 N butterflies, a 3 * 2k * k * N multiply-add
+    contraction and a 6-modmul CRT per output coefficient (2kN of them)."""
     k, n = ctx.k, ctx.n
     logn = n.bit_length() - 1
-    modmuls = (k * k + 2 * k) * ((n // 2) * logn + n) + 2 * k * k * n
-    return {"modmuls": modmuls, "key_bytes": 2 * k * k * n * 4, "ct_bytes": 3 * k * n * 4}
+    ref = (k * k + 2 * k) * ((n // 2) * logn + n) + 2 * k * k * n
+    out = {"modmuls": ref, "key_bytes": 2 * k * k * n * 4, "ct_bytes": 3 * k * n * 4,
+           "aux": bool(getattr(ctx, "ks_aux", False))}
+    if out["aux"]:
+        out.update(butterflies=9 * k * (n // 2) * logn, macs=6 * k * k * n, crt_modmuls=12 * k * n,
+                   key_bytes=6 * k * k * n * 4,
+                   # digits in (k rows), X out + in (3k + 3k), Y out + in (6k + 6k), 2k rows out
+                   ct_bytes=21 * k * n * 4)
+    return out
 
 
 def run_ours(args, rank, local_rank, world):
@@ -227,27 +239,51 @@ def run_ours(args, rank, local_rank, world):
         work = _ks_work(be.ctx)
         avg_launch_ms = ks_ms / max(1, ks_launches)
         cts_per_launch = ks_cts / max(1, ks_launches)
-        achieved = work["modmuls"] * cts_per_launch / (avg_launch_ms * 1e-3) / 1e12
-        traffic = _ncu_traffic(ks_cts / max(1, ks_launches))
+        t_ct = avg_launch_ms * 1e-3 / max(1e-9, cts_per_launch)  # seconds per key switch
+        bf_peak = peak["shoup_butterfly"]
+        traffic = _ncu_traffic(cts_per_launch, work["aux"])
         counts = workload_op_counts(cfg)
-        roofline = {
-            "kernel": "k_keyswitch<14,4> (fused digit NTT -> MAC -> iNTT)",
-            "bound": "int-pipe (IMAD)", "unit": "Tmodmul/s",
-            "achieved": round(achieved, 3), "peak": round(peak["shoup_butterfly"], 3),
-            "frac": round(achieved / peak["shoup_butterfly"], 4),
-            "peak_source": "measured live by tools/probe_int (lazy Shoup butterfly = 1 modmul "
-                           "+ 3 adds, 8 independent chains/thread, whole GPU)",
-            "work_per_ct": f"(k^2+2k)((N/2)log2N+N)+2k^2N = {work['modmuls']} modmuls",
-            "avg_launch_ms": round(avg_launch_ms, 4), "cts_per_launch": round(cts_per_launch, 1),
-            "launches_in_step": ks_launches / args.steps,
-            "ks_share_of_step": round(ks_ms / args.steps / step_ms, 4),
-            "traffic": traffic,
-            "hbm_view": {"algorithmic_bytes_per_launch": int(
-                work["key_bytes"] + work["ct_bytes"] * cts_per_launch),
-                "achieved_GBs": round((work["key_bytes"] + work["ct_bytes"] * cts_per_launch)
-                                      / (avg_launch_ms * 1e-3) / 1e9, 1),
-                "peak_GBs": _hbm_peak()},
-        }
+        hbm = {"algorithmic_bytes_per_launch": int(work["key_bytes"] + work["ct_bytes"]
+                                                   * cts_per_launch),
+               "achieved_GBs": round((work["key_bytes"] + work["ct_bytes"] * cts_per_launch)
+                                     / (avg_launch_ms * 1e-3) / 1e9, 1),
+               "peak_GBs": _hbm_peak()}
+        common = {"avg_launch_ms": round(avg_launch_ms, 4),
+                  "cts_per_launch": round(cts_per_launch, 1),
+                  "launches_in_step": ks_launches / args.steps,
+                  "ks_share_of_step": round(ks_ms / args.steps / step_ms, 4),
+                  "traffic": traffic, "hbm_view": hbm,
+                  "reference_formulation_Tmodmul_s": round(work["modmuls"] / t_ct / 1e12, 3)}
+        if work["aux"]:
+            # butterfly-equivalent ops: transforms + CRT at the butterfly rate,
+            # the contraction at the measured 64-bit multiply-add rate
+            equiv = (work["butterflies"] + work["crt_modmuls"]
+                     + work["macs"] * bf_peak / peak["mad_wide_acc"])
+            achieved = equiv / t_ct / 1e12
+            roofline = {
+                "kernel": "aux-basis key switch: k_ksa_fwd (3k NTTs) -> k_ksa_mac (64-bit "
+                          "contraction) -> k_ksa_inv (6k iNTTs + exact CRT)",
+                "bound": "int-pipe (IMAD)", "unit": "Tmodmul/s (butterfly-equivalent)",
+                "achieved": round(achieved, 3), "peak": round(bf_peak, 3),
+                "frac": round(achieved / bf_peak, 4),
+                "peak_source": "measured live by tools/probe_int: lazy Shoup butterfly "
+                               f"{bf_peak:.2f} T/s, mad.wide.u32 {peak['mad_wide_acc']:.2f} T/s",
+                "work_per_ct": (f"{work['butterflies']} butterflies (9k transforms) + "
+                                f"{work['macs']} multiply-adds (6k^2 N) + {work['crt_modmuls']} "
+                                "CRT modmuls"),
+                "ideal_us_per_ct": round(equiv / bf_peak / 1e6, 3),
+                "measured_us_per_ct": round(t_ct * 1e6, 3), **common}
+        else:
+            achieved = work["modmuls"] / t_ct / 1e12
+            roofline = {
+                "kernel": "k_keyswitch<14,4> (fused digit NTT -> MAC -> iNTT)",
+                "bound": "int-pipe (IMAD)", "unit": "Tmodmul/s",
+                "achieved": round(achieved, 3), "peak": round(bf_peak, 3),
+                "frac": round(achieved / bf_peak, 4),
+                "peak_source": "measured live by tools/probe_int (lazy Shoup butterfly = 1 modmul "
+                               "+ 3 adds, 8 independent chains/thread, whole GPU)",
+                "work_per_ct": f"(k^2+2k)((N/2)log2N+N)+2k^2N = {work['modmuls']} modmuls",
+                **common}
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = _cpu_baseline_single(params, counts)
@@ -285,8 +321,10 @@ def _int_peak() -> dict:
     sys.path.insert(0, str(ROOT / "tools"))
     from probe_int import measure
 
-    names = ["imad", "imad_hi", "imad_wide", "iadd3", "shoup_butterfly"]
-    out = {n: measure(k) / 1e12 for k, n in enumerate(names) if n != "iadd3"}
+    names = ["imad", "imad_hi", "imad_wide", "iadd3", "shoup_butterfly", "shoup_butterfly64",
+             "mad_wide_acc"]
+    out = {n: measure(k) / 1e12 for k, n in enumerate(names)
+           if n not in ("iadd3", "shoup_butterfly64")}
     torch.cuda.synchronize()
     return out
 
@@ -298,10 +336,11 @@ def _hbm_peak():
         return 6650.0
 
 
-def _ncu_traffic(cts_per_launch=None):
-    """dram bytes (read + write) per k_keyswitch launch from the committed ncu
-    capture (profiles/ks_traffic.json), scaled to this run's average launch."""
-    p = ROOT / "profiles" / "ks_traffic.json"
+def _ncu_traffic(cts_per_launch=None, aux=False):
+    """dram bytes (read + write) per key-switch launch from the committed ncu
+    capture (profiles/ks_aux_traffic.json for the aux-basis kernels,
+    profiles/ks_traffic.json for k_keyswitch), scaled to this run's launch."""
+    p = ROOT / "profiles" / ("ks_aux_traffic.json" if aux else "ks_traffic.json")
     if not p.exists():
         return None
     try:

@@ -203,6 +203,29 @@ int hefv_accumulate_rows(hefv_ctx* ctx, const uint32_t* rows, const int32_t* seg
 int hefv_add_part0(hefv_ctx* ctx, uint32_t* rows, int64_t row_stride, const int32_t* slot,
                    const uint32_t* add, int64_t P, void* stream);
 
+/* ---- key switch through an auxiliary basis (K4, second formulation) ----
+ * The same result as hefv_keyswitch -- d_j = (sum_i c_i (*) B_ji) mod p_j,
+ * fv.py:205-217 -- computed exactly as an integer convolution in the basis of
+ * three ~28-bit NTT primes primes32[aux_base .. aux_base+3) and reduced mod
+ * p_j: 3k forward + 6k inverse transforms instead of k^2 + 2k.
+ * hefv_ks_aux_setup: after hefv_fv_setup; validates the bound
+ *   8 k N max(q_j)^2 < a_0 a_1 a_2 and k a_t^2 < 2^62 (k <= 24).
+ * hefv_ks_aux_key: switch key (k, k, N) Montgomery device order (as for
+ *   hefv_keyswitch) -> kaux (3, 2k, k, N) = NTT_{a_t}(iNTT_j(K_ji)), parts
+ *   [body j | mask j].
+ * hefv_keyswitch_aux: arguments as hefv_keyswitch, plus scratch of
+ *   scratch_cts * 9 k N words (ciphertexts are processed in chunks of
+ *   scratch_cts). */
+int hefv_ks_aux_setup(hefv_ctx* ctx, int32_t aux_base);
+int hefv_ks_aux_key(hefv_ctx* ctx, const uint32_t* kbody, const uint32_t* kmask, uint32_t* kaux,
+                    void* stream);
+int hefv_keyswitch_aux(hefv_ctx* ctx, const uint32_t* kaux, const uint32_t* digits,
+                       int64_t dig_stride, uint32_t* out0, uint32_t* out1, int64_t out_stride,
+                       const int32_t* slot, const uint32_t* adA0, const uint32_t* adA1,
+                       int64_t adA_stride, const uint32_t* adB0, const uint32_t* adB1,
+                       int64_t adB_stride, uint32_t* scratch, int64_t scratch_cts, int64_t B,
+                       void* stream);
+
 /* ---- 64-bit RNS key switch (config-4 microbench; _keyswitch_apply,
  * fv.py:205-217, for 50-62-bit primes) --------------------------------------
  * Context: the L 64-bit primes of the context.  kbody/kmask: (L, L, N) =

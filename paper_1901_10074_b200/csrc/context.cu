@@ -224,6 +224,7 @@ void hefv_ctx_destroy(hefv_ctx* c) {
   cudaFree(c->d_mp);
   cudaFree(c->d_delta);
   cudaFree(c->d_tmod);
+  cudaFree(c->d_ksa_j);
   delete c;
 }
 

@@ -8,6 +8,18 @@
 
 #include "modarith.cuh"
 
+namespace hefv {
+// aux-basis key switch constants (ks_aux.cu)
+struct KsaJ {
+  uint2 c[3];      // (A / a_t) mod p_j, Shoup pair
+  uint32_t e[4];   // (-v A) mod p_j, v = 0..3
+};
+struct KsaT {
+  uint2 inv[3];    // (A / a_t)^-1 mod a_t, Shoup pair
+  uint32_t qs[3];  // floor(2^46 / a_t): y * 2^14 / a_t = umulhi(y, qs)
+};
+}  // namespace hefv
+
 struct hefv_ctx {
   int log_n = 0;
   int n = 0;
@@ -48,7 +60,13 @@ struct hefv_ctx {
   uint32_t* d_tmod = nullptr;    // t mod q_j (k)
   int ks_prefetch = 0;  // key switch: bulk-copy prefetch of the next digit into the tile (measured slower)
   int ks_e32 = 0;   // key switch at N = 2^14: 32 words per thread (512 threads)
-  int ks_tmem = 0;  // key switch: 0 plain, 1 TMEM mask acc (E=16), 2 both accs in TMEM (E=32)
+  int ks_tmem = 0;
+  // aux-basis key switch (hefv_ks_aux_setup): three ~28-bit NTT primes at
+  // primes32[ksa_base, ksa_base + 3)
+  bool ksa_ready = false;
+  int ksa_base = -1;
+  hefv::KsaJ* d_ksa_j = nullptr;
+  hefv::KsaT ksa_t{};  // key switch: 0 plain, 1 TMEM mask acc (E=16), 2 both accs in TMEM (E=32)
 };
 
 namespace hefv {

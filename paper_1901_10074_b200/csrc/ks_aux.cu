@@ -1,0 +1,537 @@
+// Key switch through an auxiliary basis (K4, second formulation).
+//
+// The reference's _keyswitch_apply (fv.py:205-217) computes, for every target
+// prime j,
+//     d_j = iNTT_j( sum_i NTT_j(c_i mod p_j) * K_ji )   mod p_j,
+// i.e. d_j = (sum_i c_i (*) B_ji) mod p_j, where (*) is the negacyclic
+// product, c_i in [0, p_i) are the digit limbs and B_ji = iNTT_j(K_ji) in
+// [0, p_j) the coefficient form of the stored key.  That integer sum is
+// bounded by k N max(p)^2 < 2^80 at the FV sizes, so it can be computed
+// EXACTLY in a basis of three ~28-bit NTT primes a_0..a_2 (product A > 2^83)
+// and reduced mod p_j afterwards -- the same canonical residues, with
+//     3k forward NTTs (each digit once per a_t) instead of k^2,
+//     3 * 2k inverse NTTs                        instead of 2k,
+// and a pointwise MAC over digits that is a small dense contraction per
+// evaluation point (done here with 64-bit integer multiply-accumulates).
+//
+//   phase 1  k_ksa_fwd : X[b][t][i]    = NTT_{a_t}(c_i)                (device order)
+//   phase 2  k_ksa_mac : Y[b][t][jp]   = sum_i X[b][t][i] * Kaux[t][jp][i]   mod a_t
+//   phase 3  k_ksa_inv : r_t = iNTT_{a_t}(Y[b][t][jp]);  exact CRT over t:
+//            y_t = r_t (A/a_t)^-1 mod a_t,  v = rint(sum_t y_t / a_t),
+//            d = sum_t y_t (A/a_t) - v A   (the centred integer),  out = d mod p_j
+//            + the caller's epilogue addends.
+// v is exact from a 2^-14 fixed-point sum because |d| / A < 2^-3: the
+// fractional part of sum y_t / a_t is within 1/8 of an integer.
+//
+// Kaux[t][part*k + j][i] = NTT_{a_t}(B_ji) (body part 0, mask part 1) is built
+// once per switch key by hefv_ks_aux_key.
+#include <cmath>
+
+#include "../../include/hefv.h"
+#include "internal.h"
+#include "kcommon.cuh"
+#include "ntt.cuh"
+
+namespace hefv {
+
+constexpr int KSA_FWD_CTS = 8;   // ciphertexts per CTA, phase 1
+constexpr int KSA_INV_CTS = 8;   // ciphertexts per CTA, phase 3
+constexpr int KSA_MAC_CTS = 128;  // ciphertexts per CTA, phase 2 (key tile reuse)
+constexpr int KSA_KMAX = 24;     // digits held in registers by phase 2
+
+__device__ __forceinline__ uint32_t shoup_canon(uint32_t x, uint2 w, uint32_t p) {
+  const uint32_t r = Mod32::mul_shoup(x, w.x, w.y, p);
+  return r >= p ? r - p : r;
+}
+
+// "Tiled" point layout of a (k, N) stack: [N/32][k][32] -- the k values of a
+// 32-point tile are one contiguous 128k-byte block, which phase 2 streams
+// with one coalesced word per thread.  Row-layout registers (E consecutive
+// points per thread, E = 16) land as one 64-byte run.
+template <int LOGN, int LOGE>
+__device__ __forceinline__ void store_tiled(uint32_t* __restrict__ base, int k, int i, int tid,
+                                            const uint32_t* v) {
+  constexpr int E = 1 << LOGE;
+  static_assert(E <= 32 && 32 % E == 0, "row runs must stay inside one tile");
+  const int p0 = tid * E;
+  uint4* d = reinterpret_cast<uint4*>(base + ((size_t)(p0 >> 5) * k + i) * 32 + (p0 & 31));
+#pragma unroll
+  for (int q = 0; q < E / 4; ++q) d[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+}
+
+__device__ __forceinline__ void cp_async4(uint32_t* dst_smem, const uint32_t* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst_smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int PENDING>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(PENDING) : "memory");
+}
+
+// ---- phase 1: digits -> aux-basis NTTs --------------------------------------
+template <int LOGN, int LOGE>
+__global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
+    k_ksa_fwd(const uint32_t* __restrict__ digits, int64_t dig_stride, uint32_t* __restrict__ X,
+              int64_t B, int k, int aux_base, const uint2* __restrict__ tw_all,
+              const Prime32Info* __restrict__ info) {
+  typedef Geo<LOGN, LOGE> G_;
+  constexpr int E = G_::E;
+  constexpr int NT = G_::NT;
+  constexpr int N = G_::N;
+  constexpr int NTW = 1 << (LOGN - G_::RLAST);
+  extern __shared__ __align__(16) unsigned char smraw[];
+  uint2* tws = reinterpret_cast<uint2*>(smraw);
+  uint32_t* sm = reinterpret_cast<uint32_t*>(tws + NTW);
+  const int t = blockIdx.x / k;
+  const int i = blockIdx.x - t * k;
+  const int tid = threadIdx.x;
+  const Prime32Info inf = info[aux_base + t];
+  const Mod32 md{inf.p, 2 * inf.p};
+  const uint2* twg = tw_all + (size_t)(aux_base + t) * N;
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(twg);
+    uint4* dst = reinterpret_cast<uint4*>(tws);
+    for (int q = tid; q < NTW / 2; q += NT) dst[q] = __ldg(src + q);
+  }
+  __syncthreads();
+  const int64_t bbeg = (int64_t)blockIdx.y * KSA_FWD_CTS;
+  const int64_t bend = min(B, bbeg + KSA_FWD_CTS);
+  for (int64_t b = bbeg; b < bend; ++b) {
+    const uint32_t* src = digits + b * dig_stride + (size_t)i * N;
+    uint32_t x[E];
+    // c_i < p_i < 2^30 <= 4 a_t: a valid lazy input
+#pragma unroll
+    for (int e = 0; e < E; ++e) x[e] = ld_stream(src + tid + e * NT);
+    cta_fwd<LOGN, LOGE, Mod32>(md, x, sm, tws, twg, NoHook(), LOGN - G_::RLAST);
+#pragma unroll
+    for (int e = 0; e < E; ++e) x[e] = md.canon4(x[e]);
+    store_tiled<LOGN, LOGE>(X + ((size_t)b * 3 + t) * k * (size_t)N, k, i, tid, x);
+  }
+}
+
+// ---- phase 2: per-point contraction over digits ----------------------------
+// CTA = (aux prime t, 32-point tile m); warp w = target prime j, lane =
+// point.  Each thread keeps its point's body and mask key words of every
+// digit in registers (2K words); the CTA streams the ciphertexts' digit tiles
+// (k x 32 words, one word per thread) through a KSA_STAGES-deep cp.async
+// ring in shared memory, and every tile word feeds two 64-bit multiply-adds.
+constexpr int KSA_STAGES = 4;
+
+__device__ __forceinline__ void mad_wide(uint64_t& acc, uint32_t a, uint32_t b) {
+  asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc) : "r"(a), "r"(b));
+}
+
+// s mod a for s < 2^62 with 32-bit operations: s = hi 2^32 + lo,
+// hi 2^32 = hi * R (R = 2^32 mod a, Shoup), lo by a 32-bit Barrett step.
+struct Red64 {
+  uint32_t a, r, rsh, mu;  // a; 2^32 mod a; floor(R 2^32 / a); floor(2^32 / a)
+  __device__ __forceinline__ uint32_t operator()(uint64_t s) const {
+    const uint32_t hi = (uint32_t)(s >> 32), lo = (uint32_t)s;
+    const uint32_t h = Mod32::mul_shoup(hi, r, rsh, a);          // [0, 2a)
+    const uint32_t q = __umulhi(lo, mu);
+    const uint32_t l = lo - q * a;                               // [0, 2a)
+    uint32_t v = h + l;                                          // [0, 4a)
+    v = min(v, v - 2 * a);
+    return min(v, v - a);
+  }
+};
+
+// K: digits contracted per point (compile time; rows k..K-1 of the ring hold
+// stale words and meet zero key words).
+template <int K>
+__global__ void __launch_bounds__(32 * K, 1)
+    k_ksa_mac(const uint32_t* __restrict__ X, const uint32_t* __restrict__ kaux,
+              uint32_t* __restrict__ Y, int64_t B, int k, int log_n, int aux_base,
+              const Prime32Info* __restrict__ info) {
+  __shared__ __align__(16) uint32_t ring[KSA_STAGES][K * 32];
+  const int n = 1 << log_n;
+  const int tiles = n >> 5;
+  const int t = blockIdx.x / tiles;
+  const int m = blockIdx.x - t * tiles;
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const bool active = w < k;
+  const int j = active ? w : 0;
+  const uint32_t a = info[aux_base + t].p;
+  Red64 red;
+  red.a = a;
+  red.r = (uint32_t)((1ull << 32) % a);
+  red.rsh = (uint32_t)(((uint64_t)red.r << 32) / a);
+  red.mu = (uint32_t)((1ull << 32) / a);
+  uint32_t kb[K], km[K];
+  const size_t kstride = (size_t)k * k * n;  // body -> mask rows of the same t
+  const uint32_t* ks = kaux + (((size_t)t * 2 * k + j) * tiles + m) * k * 32 + lane;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    kb[i] = i < k ? __ldg(ks + 32 * i) : 0u;
+    km[i] = i < k ? __ldg(ks + kstride + 32 * i) : 0u;
+  }
+  const int64_t bbeg = (int64_t)blockIdx.y * KSA_MAC_CTS;
+  const int64_t bend = min(B, bbeg + KSA_MAC_CTS);
+  const int nb = (int)(bend - bbeg);
+  const bool copier = threadIdx.x < k * 32;
+  // X tile of ciphertext b: (((b * 3 + t) * tiles + m) * k) * 32 words, k*32 long
+  const size_t xstride = (size_t)3 * tiles * k * 32;
+  const uint32_t* xsrc = X + (((size_t)bbeg * 3 + t) * tiles + m) * k * 32 + threadIdx.x;
+#pragma unroll
+  for (int s = 0; s < KSA_STAGES - 1; ++s) {
+    if (copier && s < nb) cp_async4(&ring[s][threadIdx.x], xsrc + s * xstride);
+    cp_async_commit();
+  }
+  xsrc += (KSA_STAGES - 1) * xstride;
+  uint32_t* yb = Y + (((size_t)bbeg * 3 + t) * 2 * k + j) * (size_t)n + (m << 5) + lane;
+  const size_t ymask = (size_t)k * n;
+  const size_t ystride = (size_t)3 * 2 * k * n;
+  for (int r = 0; r < nb; ++r) {
+    cp_async_wait<KSA_STAGES - 2>();
+    __syncthreads();  // tile r visible to all; slot (r - 1) % S free for reuse
+    if (copier && r + KSA_STAGES - 1 < nb)
+      cp_async4(&ring[(r + KSA_STAGES - 1) % KSA_STAGES][threadIdx.x], xsrc);
+    cp_async_commit();
+    xsrc += xstride;
+    const uint32_t* xt = ring[r % KSA_STAGES] + lane;
+    uint64_t b0 = 0, b1 = 0, m0 = 0, m1 = 0;
+#pragma unroll
+    for (int i = 0; i + 1 < K; i += 2) {
+      const uint32_t x0 = xt[32 * i], x1 = xt[32 * (i + 1)];
+      mad_wide(b0, x0, kb[i]);
+      mad_wide(m0, x0, km[i]);
+      mad_wide(b1, x1, kb[i + 1]);
+      mad_wide(m1, x1, km[i + 1]);
+    }
+    if constexpr (K & 1) {
+      const uint32_t x0 = xt[32 * (K - 1)];
+      mad_wide(b0, x0, kb[K - 1]);
+      mad_wide(m0, x0, km[K - 1]);
+    }
+    if (active) {
+      yb[0] = red(b0 + b1);
+      yb[ymask] = red(m0 + m1);
+    }
+    yb += ystride;
+  }
+}
+
+// ---- phase 3: three inverse NTTs + exact CRT + epilogue ---------------------
+// CTA = (output row jp = part * k + j, KSA_INV_CTS ciphertexts).  The inverse
+// twiddles of the three aux primes' full passes sit in shared memory (the
+// last pass reads its entries through L1); the quotient estimate
+// sum_t y_t / a_t is accumulated as 2^14-scaled fixed point (16 bits per
+// coefficient, error < 3 * 2^-14, far inside the 3/8 rounding margin).
+template <int LOGN, int LOGE>
+__global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
+    k_ksa_inv(const uint32_t* __restrict__ Y, uint32_t* out0, uint32_t* out1, int64_t out_stride,
+              const int32_t* __restrict__ slot, const uint32_t* __restrict__ adA0,
+              const uint32_t* __restrict__ adA1, int64_t adA_stride, const uint32_t* adB0,
+              const uint32_t* adB1, int64_t adB_stride, int64_t B, int k, int aux_base,
+              const uint2* __restrict__ itw_all, const Prime32Info* __restrict__ info,
+              const KsaJ* __restrict__ cj, KsaT ct) {
+  typedef Geo<LOGN, LOGE> G_;
+  constexpr int E = G_::E;
+  constexpr int NT = G_::NT;
+  constexpr int N = G_::N;
+  constexpr int NTW = 1 << (LOGN - G_::RLAST);
+  static_assert(E % 8 == 0, "fixed-point quotient words move 8 at a time");
+  extern __shared__ __align__(16) unsigned char smraw[];
+  uint2* tws = reinterpret_cast<uint2*>(smraw);                  // [3][NTW]
+  uint32_t* sm = reinterpret_cast<uint32_t*>(tws + 3 * NTW);
+  uint4* vsum = reinterpret_cast<uint4*>(sm + ((spad_size(N) + 3) & ~3));  // [E/8][NT] x 8 u16
+  const int jp = blockIdx.x;
+  const int part = jp >= k ? 1 : 0;
+  const int j = jp - part * k;
+  const int tid = threadIdx.x;
+  const Prime32Info pj = info[j];
+  const Mod32 mj{pj.p, 2 * pj.p};
+  const KsaJ cc = cj[j];
+  for (int t = 0; t < 3; ++t) {
+    const uint4* src = reinterpret_cast<const uint4*>(itw_all + (size_t)(aux_base + t) * N);
+    uint4* dst = reinterpret_cast<uint4*>(tws + t * NTW);
+    for (int q = tid; q < NTW / 2; q += NT) dst[q] = __ldg(src + q);
+  }
+  __syncthreads();
+  const int64_t bbeg = (int64_t)blockIdx.y * KSA_INV_CTS;
+  const int64_t bend = min(B, bbeg + KSA_INV_CTS);
+  for (int64_t b = bbeg; b < bend; ++b) {
+    uint32_t acc[E], x[E];
+#pragma unroll 1
+    for (int t = 0; t < 3; ++t) {
+      const Prime32Info pa = info[aux_base + t];
+      const Mod32 ma{pa.p, 2 * pa.p};
+      load_row_vec<LOGN, LOGE>(Y + (((size_t)b * 3 + t) * 2 * k + jp) * N, tid, x);
+      cta_inv<LOGN, LOGE, Mod32>(ma, x, sm, tws + t * NTW, pa.ninv, pa.wn,
+                                 itw_all + (size_t)(aux_base + t) * N);
+      // constant selects (no dynamic indexing of the by-value parameters)
+      const uint2 inv = t == 0 ? ct.inv[0] : (t == 1 ? ct.inv[1] : ct.inv[2]);
+      const uint2 c = t == 0 ? cc.c[0] : (t == 1 ? cc.c[1] : cc.c[2]);
+      const uint32_t qs = t == 0 ? ct.qs[0] : (t == 1 ? ct.qs[1] : ct.qs[2]);
+#pragma unroll
+      for (int q = 0; q < E / 8; ++q) {
+        uint4 vv = t ? vsum[q * NT + tid] : make_uint4(0u, 0u, 0u, 0u);
+        uint32_t* vw = reinterpret_cast<uint32_t*>(&vv);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const int e = 8 * q + r;
+          const uint32_t y = shoup_canon(ma.subp(x[e]), inv, pa.p);
+          // y * 2^14 / a_t, rounded down (< 2^14): 16-bit lanes never carry
+          const uint32_t f = __umulhi(y, qs);
+          vw[r >> 1] += (r & 1) ? (f << 16) : f;
+          const uint32_t m = Mod32::mul_shoup(y, c.x, c.y, pj.p);  // [0, 2 p_j)
+          acc[e] = t ? mj.sub2p(acc[e] + m) : m;
+        }
+        vsum[q * NT + tid] = vv;
+      }
+    }
+    const int64_t s = slot ? (int64_t)slot[b] : b;
+    uint32_t* o = (part ? out1 : out0) + s * out_stride + (size_t)j * N;
+    const uint32_t* aA = part ? adA1 : adA0;
+    const uint32_t* aB = part ? adB1 : adB0;
+    const uint32_t* a = aA ? aA + b * adA_stride + (size_t)j * N : nullptr;
+    const uint32_t* c = aB ? aB + s * adB_stride + (size_t)j * N : nullptr;
+#pragma unroll
+    for (int q = 0; q < E / 8; ++q) {
+      const uint4 vv = vsum[q * NT + tid];
+      const uint32_t* vw = reinterpret_cast<const uint32_t*>(&vv);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int e = 8 * q + r;
+        const int idx = tid + e * NT;
+        const uint32_t f = (r & 1) ? (vw[r >> 1] >> 16) : (vw[r >> 1] & 0xffffu);
+        const uint32_t v = ((f + (1u << 13)) >> 14) & 3u;  // rint(sum_t y_t / a_t)
+        const uint32_t ev = v == 0 ? cc.e[0] : (v == 1 ? cc.e[1] : (v == 2 ? cc.e[2] : cc.e[3]));
+        uint32_t val = mj.canon4(acc[e] + ev);
+        if (a) val = mj.subp(val + a[idx]);
+        if (c) val = mj.subp(val + c[idx]);
+        o[idx] = val;
+      }
+    }
+  }
+}
+
+// ---- switch key -> aux-basis form ------------------------------------------
+// CTA = (part, j, i): B_ji = iNTT_j(mont^-1(K_ji)), then NTT_{a_t} for t < 3.
+template <int LOGN, int LOGE>
+__global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
+    k_ksa_key(const uint32_t* __restrict__ kbody, const uint32_t* __restrict__ kmask,
+              uint32_t* __restrict__ kaux, int k, int aux_base, const uint2* __restrict__ tw_all,
+              const uint2* __restrict__ itw_all, const Prime32Info* __restrict__ info) {
+  typedef Geo<LOGN, LOGE> G_;
+  constexpr int E = G_::E;
+  constexpr int N = G_::N;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  uint32_t* sm = reinterpret_cast<uint32_t*>(smraw);
+  const int i = blockIdx.x;
+  const int j = blockIdx.y;
+  const int part = blockIdx.z;
+  const int tid = threadIdx.x;
+  const Prime32Info pj = info[j];
+  const Mod32 mj{pj.p, 2 * pj.p};
+  uint32_t x[E], y[E];
+  load_row_vec<LOGN, LOGE>((part ? kmask : kbody) + ((size_t)j * k + i) * N, tid, x);
+  // Montgomery form x 2^32 -> x: REDC(x) in [0, 2p) -> canonical
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const uint32_t m = x[e] * pj.pinv_neg;
+    const uint64_t s = (uint64_t)x[e] + (uint64_t)m * pj.p;
+    x[e] = mj.subp((uint32_t)(s >> 32));
+  }
+  cta_inv<LOGN, LOGE, Mod32>(mj, x, sm, itw_all + (size_t)j * N, pj.ninv, pj.wn);
+#pragma unroll
+  for (int e = 0; e < E; ++e) x[e] = mj.subp(x[e]);  // B_ji coefficients in [0, p_j)
+#pragma unroll 1
+  for (int t = 0; t < 3; ++t) {
+    const Prime32Info pa = info[aux_base + t];
+    const Mod32 ma{pa.p, 2 * pa.p};
+#pragma unroll
+    for (int e = 0; e < E; ++e) y[e] = x[e];  // < 2^30 <= 4 a_t
+    cta_fwd<LOGN, LOGE, Mod32>(ma, y, sm, tw_all + (size_t)(aux_base + t) * N);
+#pragma unroll
+    for (int e = 0; e < E; ++e) y[e] = ma.canon4(y[e]);
+    store_tiled<LOGN, LOGE>(kaux + (((size_t)t * 2 + part) * k + j) * k * (size_t)N, k, i, tid, y);
+  }
+}
+
+template <int LOGN>
+static int run_ksa(hefv_ctx* c, const uint32_t* kaux, const uint32_t* dig, int64_t ds,
+                   uint32_t* o0, uint32_t* o1, int64_t os, const int32_t* slot,
+                   const uint32_t* a0, const uint32_t* a1, int64_t as, const uint32_t* b0,
+                   const uint32_t* b1, int64_t bs, uint32_t* scratch, int64_t scratch_cts,
+                   int64_t B, cudaStream_t st) {
+  constexpr int LE = 4;
+  typedef Geo<LOGN, LE> G_;
+  const int k = c->k;
+  const int64_t n = c->n;
+  const int ab = c->ksa_base;
+  auto kf = k_ksa_fwd<LOGN, LE>;
+  auto ki = k_ksa_inv<LOGN, LE>;
+  const size_t tile = (size_t)((spad_size(G_::N) + 3) & ~3) * 4;
+  const size_t smf = (size_t)(1 << (LOGN - G_::RLAST)) * sizeof(uint2) + tile;
+  const size_t smi = (size_t)3 * (1 << (LOGN - G_::RLAST)) * sizeof(uint2) + tile +
+                     (size_t)G_::N * 2;
+  HEFV_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smf));
+  HEFV_CUDA(cudaFuncSetAttribute(ki, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smi));
+  const int64_t chunk = scratch_cts < B ? scratch_cts : B;
+  uint32_t* X = scratch;
+  uint32_t* Y = scratch + chunk * 3 * k * n;
+  for (int64_t c0 = 0; c0 < B; c0 += chunk) {
+    const int64_t nb = (B - c0) < chunk ? (B - c0) : chunk;
+    {
+      dim3 grid((unsigned)(3 * k), (unsigned)((nb + KSA_FWD_CTS - 1) / KSA_FWD_CTS));
+      kf<<<grid, G_::NT, smf, st>>>(dig + c0 * ds, ds, X, nb, k, ab, c->d_tw32, c->d_info32);
+      HEFV_LAUNCH_CHECK("k_ksa_fwd");
+    }
+    {
+      dim3 grid((unsigned)(3 * (n >> 5)), (unsigned)((nb + KSA_MAC_CTS - 1) / KSA_MAC_CTS));
+      if (k == 22)
+        k_ksa_mac<22><<<grid, 32 * 22, 0, st>>>(X, kaux, Y, nb, k, c->log_n, ab, c->d_info32);
+      else if (k <= 16)
+        k_ksa_mac<16><<<grid, 32 * 16, 0, st>>>(X, kaux, Y, nb, k, c->log_n, ab, c->d_info32);
+      else
+        k_ksa_mac<KSA_KMAX><<<grid, 32 * KSA_KMAX, 0, st>>>(X, kaux, Y, nb, k, c->log_n, ab,
+                                                             c->d_info32);
+      HEFV_LAUNCH_CHECK("k_ksa_mac");
+    }
+    {
+      dim3 grid((unsigned)(2 * k), (unsigned)((nb + KSA_INV_CTS - 1) / KSA_INV_CTS));
+      const int32_t* sl = slot ? slot + c0 : nullptr;
+      uint32_t* oo0 = o0;
+      uint32_t* oo1 = o1;
+      const uint32_t* bb0 = b0;
+      const uint32_t* bb1 = b1;
+      if (!slot) {  // output index = batch index: shift the bases
+        oo0 += c0 * os;
+        oo1 += c0 * os;
+        if (bb0) bb0 += c0 * bs;
+        if (bb1) bb1 += c0 * bs;
+      }
+      ki<<<grid, G_::NT, smi, st>>>(Y, oo0, oo1, os, sl, a0 ? a0 + c0 * as : nullptr,
+                                    a1 ? a1 + c0 * as : nullptr, as, bb0, bb1, bs, nb, k, ab,
+                                    c->d_itw32, c->d_info32, c->d_ksa_j, c->ksa_t);
+      HEFV_LAUNCH_CHECK("k_ksa_inv");
+    }
+  }
+  return 0;
+}
+
+}  // namespace hefv
+
+using namespace hefv;
+
+namespace {
+
+uint64_t mulmod_u64(uint64_t a, uint64_t b, uint64_t m) {
+  return (uint64_t)((unsigned __int128)a * b % m);
+}
+uint64_t powmod_u64(uint64_t a, uint64_t e, uint64_t m) {
+  uint64_t r = 1 % m;
+  a %= m;
+  while (e) {
+    if (e & 1) r = mulmod_u64(r, a, m);
+    a = mulmod_u64(a, a, m);
+    e >>= 1;
+  }
+  return r;
+}
+uint2 shoup_pair(uint32_t w, uint32_t p) {
+  return make_uint2(w, (uint32_t)(((uint64_t)w << 32) / p));
+}
+
+template <int LOGN>
+int run_ksa_key(hefv_ctx* c, const uint32_t* kb, const uint32_t* km, uint32_t* kaux,
+                cudaStream_t st) {
+  typedef Geo<LOGN, 4> G_;
+  auto kern = k_ksa_key<LOGN, 4>;
+  const size_t sm = (size_t)((spad_size(G_::N) + 3) & ~3) * 4;
+  HEFV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  dim3 grid((unsigned)c->k, (unsigned)c->k, 2);
+  kern<<<grid, G_::NT, sm, st>>>(kb, km, kaux, c->k, c->ksa_base, c->d_tw32, c->d_itw32,
+                                 c->d_info32);
+  HEFV_LAUNCH_CHECK("k_ksa_key");
+  return 0;
+}
+
+}  // namespace
+
+#define HEFV_KSA_DISPATCH(FN, ...)                       \
+  switch (c->log_n) {                                    \
+    case 10: return FN<10>(__VA_ARGS__);                 \
+    case 11: return FN<11>(__VA_ARGS__);                 \
+    case 12: return FN<12>(__VA_ARGS__);                 \
+    case 13: return FN<13>(__VA_ARGS__);                 \
+    case 14: return FN<14>(__VA_ARGS__);                 \
+    default: return fail("aux key switch: N must be 2^10 .. 2^14"); \
+  }
+
+extern "C" {
+
+int hefv_ks_aux_setup(hefv_ctx* c, int32_t aux_base) {
+  if (!c || !c->fv_ready) return fail("hefv_ks_aux_setup: context without FV setup");
+  const int k = c->k;
+  if (k < 1 || k > KSA_KMAX) return fail("hefv_ks_aux_setup: needs 1 <= k <= 24 q primes");
+  if (aux_base < c->k + c->a || aux_base + 3 > c->n32)
+    return fail("hefv_ks_aux_setup: aux primes must follow the FV primes in the context");
+  if (c->log_n < 10 || c->log_n > 14) return fail("hefv_ks_aux_setup: N must be 2^10 .. 2^14");
+  uint32_t a[3];
+  unsigned __int128 A = 1;
+  for (int t = 0; t < 3; ++t) {
+    a[t] = c->primes32[aux_base + t];
+    if (a[t] <= (1u << 28)) return fail("hefv_ks_aux_setup: aux primes must exceed 2^28");
+    // digit MAC: k products < a^2 summed in 64 bits, Barrett needs < 2^62
+    if ((unsigned __int128)k * a[t] * a[t] >= ((unsigned __int128)1 << 62))
+      return fail("hefv_ks_aux_setup: aux primes too large for the 64-bit digit MAC");
+    A *= a[t];
+  }
+  uint32_t pmax = 0;
+  for (int j = 0; j < k; ++j) pmax = c->primes32[j] > pmax ? c->primes32[j] : pmax;
+  // |sum_i c_i (*) B_ji| < k N pmax^2; need < A / 8 for the rounding of v
+  const unsigned __int128 bound = (unsigned __int128)8 * k * (uint64_t)c->n * pmax * pmax;
+  if (bound >= A) return fail("hefv_ks_aux_setup: aux basis too small for this (k, N)");
+  KsaT ct;
+  for (int t = 0; t < 3; ++t) {
+    const uint32_t u = a[(t + 1) % 3], v = a[(t + 2) % 3];
+    const uint64_t rest = mulmod_u64(u, v, a[t]);
+    ct.inv[t] = shoup_pair((uint32_t)powmod_u64(rest, a[t] - 2, a[t]), a[t]);
+    ct.qs[t] = (uint32_t)((1ull << 46) / a[t]);
+  }
+  std::vector<KsaJ> cj(k);
+  for (int j = 0; j < k; ++j) {
+    const uint32_t p = c->primes32[j];
+    for (int t = 0; t < 3; ++t) {
+      const uint32_t u = a[(t + 1) % 3], v = a[(t + 2) % 3];
+      cj[j].c[t] = shoup_pair((uint32_t)mulmod_u64(u % p, v % p, p), p);
+    }
+    const uint64_t Am = mulmod_u64(mulmod_u64(a[0] % p, a[1] % p, p), a[2] % p, p);
+    for (int vv = 0; vv < 4; ++vv) cj[j].e[vv] = (uint32_t)((p - mulmod_u64(vv, Am, p)) % p);
+  }
+  cudaFree(c->d_ksa_j);
+  c->d_ksa_j = nullptr;
+  HEFV_CUDA(cudaMalloc(&c->d_ksa_j, cj.size() * sizeof(KsaJ)));
+  HEFV_CUDA(cudaMemcpy(c->d_ksa_j, cj.data(), cj.size() * sizeof(KsaJ), cudaMemcpyHostToDevice));
+  c->ksa_t = ct;
+  c->ksa_base = aux_base;
+  c->ksa_ready = true;
+  return 0;
+}
+
+int hefv_ks_aux_key(hefv_ctx* c, const uint32_t* kbody, const uint32_t* kmask, uint32_t* kaux,
+                    void* stream) {
+  if (!c || !c->ksa_ready) return fail("hefv_ks_aux_key: aux key switch not set up");
+  cudaStream_t st = as_stream(stream);
+  HEFV_KSA_DISPATCH(run_ksa_key, c, kbody, kmask, kaux, st)
+}
+
+int hefv_keyswitch_aux(hefv_ctx* c, const uint32_t* kaux, const uint32_t* digits,
+                       int64_t dig_stride, uint32_t* out0, uint32_t* out1, int64_t out_stride,
+                       const int32_t* slot, const uint32_t* adA0, const uint32_t* adA1,
+                       int64_t adA_stride, const uint32_t* adB0, const uint32_t* adB1,
+                       int64_t adB_stride, uint32_t* scratch, int64_t scratch_cts, int64_t B,
+                       void* stream) {
+  if (!c || !c->ksa_ready) return fail("hefv_keyswitch_aux: aux key switch not set up");
+  if (B <= 0) return 0;
+  if (scratch_cts < 1) return fail("hefv_keyswitch_aux: scratch must hold at least one ciphertext");
+  cudaStream_t st = as_stream(stream);
+  HEFV_KSA_DISPATCH(run_ksa, c, kaux, digits, dig_stride, out0, out1, out_stride, slot, adA0,
+                    adA1, adA_stride, adB0, adB1, adB_stride, scratch, scratch_cts, B, st)
+}
+
+}  // extern "C"

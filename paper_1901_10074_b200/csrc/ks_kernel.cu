@@ -50,7 +50,7 @@ constexpr int KS_CTS_PER_CTA = HEFV_KS_CTS;
 // the last pass and the MAC.
 template <int LOGN, int LOGE, bool PREFETCH = false>
 __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT,
-                                  Geo<LOGN, LOGE>::NT >= 512 ? 1 : 512 / Geo<LOGN, LOGE>::NT)
+                                  Geo<LOGN, LOGE>::NT >= 1024 ? 1 : 1024 / Geo<LOGN, LOGE>::NT)
     k_keyswitch(const uint32_t* __restrict__ kbody, const uint32_t* __restrict__ kmask,
                 const uint32_t* __restrict__ digits, int64_t dig_stride, uint32_t* out0,
                 uint32_t* out1, int64_t out_stride, const int32_t* __restrict__ slot,

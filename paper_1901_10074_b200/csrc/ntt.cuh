@@ -336,14 +336,17 @@ __device__ __forceinline__ void inv_full_pass(const M& md, typename M::T* x, int
 // Inverse transform: x in row layout (values < 2p) -> column layout
 // (natural coefficient order), values in [0, 2p).  N^{-1} is applied.
 // Exchanges run from fine (warp / group) to coarse (CTA-wide).
+// `itw_last` (optional): table the last pass reads instead of `itw` (e.g. the
+// full-pass entries staged in shared memory as `itw`, the rest from global).
 template <int LOGN, int LOGE, class M>
 __device__ __forceinline__ void cta_inv(const M& md, typename M::T* x, typename M::T* sm,
                                         const typename M::Tw* __restrict__ itw,
-                                        typename M::Tw ninv, typename M::Tw wn) {
+                                        typename M::Tw ninv, typename M::Tw wn,
+                                        const typename M::Tw* __restrict__ itw_last = nullptr) {
   typedef Geo<LOGN, LOGE> G_;
   constexpr int LOG_NT = LOGN - LOGE;
   const int tid = threadIdx.x;
-  inv_last_pass<LOGN, LOGE, M>(md, x, tid, itw, ninv, wn);
+  inv_last_pass<LOGN, LOGE, M>(md, x, tid, itw_last ? itw_last : itw, ninv, wn);
 #pragma unroll
   for (int pass = G_::NFULL - 1; pass >= 0; --pass) {
     // group of this exchange: threads sharing a pass-`pass` region

@@ -8,6 +8,8 @@
 //   kind 3: IADD3     (ALU pipe reference)
 //   kind 4: one lazy Shoup Cooley-Tukey butterfly (counted as 1 op)
 //   kind 5: one lazy 64-bit Shoup butterfly (p < 2^62; counted as 1 op)
+//   kind 6: IMAD.WIDE.U32 multiply-accumulate into 64 bits (mad.wide.u32)
+//   kind 7: DFMA (fp64 fused multiply-add)
 // Each thread runs 8 independent chains so the pipes, not latency, bound it.
 #include "../../include/hefv.h"
 #include "internal.h"
@@ -83,6 +85,51 @@ __global__ void __launch_bounds__(256) k_probe(uint32_t* out, int iters, uint32_
   if (s == 0x12345678u) out[0] = s;  // keep the work alive
 }
 
+__global__ void __launch_bounds__(256) k_probe_madwide(uint32_t* out, int iters, uint32_t seed) {
+  uint64_t acc[8];
+  uint32_t a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    acc[i] = seed + i;
+    a[i] = seed * (threadIdx.x + 1) + i * 0x9e3779b9u;
+  }
+  const uint32_t b = seed | 0x10001u;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc[i]) : "r"(a[i]), "r"(b));
+    }
+  }
+  uint64_t s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s ^= acc[i];
+  if (s == 0x12345678ull) out[0] = (uint32_t)s;
+}
+
+__global__ void __launch_bounds__(256) k_probe_dfma(uint32_t* out, int iters, uint32_t seed) {
+  double acc[8];
+  const double b = 1.0000001 + seed * 1e-9;
+  double a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    acc[i] = i;
+    a[i] = 0.5 + threadIdx.x * 1e-6 + i;
+  }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = fma(a[i], b, acc[i]);
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += acc[i];
+  if (s == 12345.678) out[0] = 1u;
+}
+
 }  // namespace hefv
 
 using namespace hefv;
@@ -109,6 +156,12 @@ extern "C" int hefv_probe_int(int32_t kind, int32_t blocks, int32_t iters, uint3
       break;
     case 5:
       k_probe64<<<blocks, 256, 0, st>>>(out, iters, 7u);
+      break;
+    case 6:
+      k_probe_madwide<<<blocks, 256, 0, st>>>(out, iters, 7u);
+      break;
+    case 7:
+      k_probe_dfma<<<blocks, 256, 0, st>>>(out, iters, 7u);
       break;
     default:
       return fail("hefv_probe_int: unknown kind");

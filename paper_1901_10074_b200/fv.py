@@ -105,7 +105,15 @@ class FvContext:
         self.slot_to_ev = slot_to_eval(n)
         if fp.t >= 1 << 62:
             raise ValueError("plain modulus must be below 2^62")
-        primes32 = self.q_primes + self.aux_primes
+        # three ~28-bit primes for the aux-basis key switch (ks_aux.cu): used
+        # when it needs fewer transforms than the per-prime one (k > 8)
+        import os
+
+        self.ks_aux = (8 < self.k <= 24 and 10 <= self.log_n <= 14
+                       and os.environ.get("HEFV_KS_AUX", "1") != "0")
+        self.ks_aux_primes = (find_ntt_primes(3, 29, 2 * n, below=int(2 ** 28.25))
+                              if self.ks_aux else [])
+        primes32 = self.q_primes + self.aux_primes + self.ks_aux_primes
         psi32 = [root_of_unity(p, n) for p in primes32]
         psi_t = root_of_unity(fp.t, n)
         arr32 = (C.c_uint32 * len(primes32))(*primes32)
@@ -137,6 +145,8 @@ class FvContext:
             c32(qc.hat_inv), mc.words, c32(mc.prod_words), c32(mc.half_words),
             c32(mc.hat_words.reshape(-1)), c32(mc.hat_inv), c32(self.delta_mod)),
             "hefv_fv_setup")
+        if self.ks_aux:
+            nat.check(lib.hefv_ks_aux_setup(h, self.k + self.a), "hefv_ks_aux_setup")
         # gadget_i mod q_j table (k x k)
         gtab = np.array([[g % p for p in self.q_primes] for g in self.gadget], dtype=np.int64)
         self.d_gadget = nat.to_device(gtab.astype(np.int32))
@@ -266,6 +276,14 @@ class SwitchKey:
         self._ctx = ctx
         self.body_dev = body_dev
         self.mask_dev = mask_dev
+        # aux-basis form for hefv_keyswitch_aux: (3, 2k, k, N)
+        self.aux_dev = None
+        if ctx.ks_aux:
+            torch = _torch()
+            self.aux_dev = torch.empty((3, 2 * ctx.k, ctx.k, ctx.n), dtype=torch.int32,
+                                       device="cuda")
+            ctx.call("hefv_ks_aux_key", body_dev.data_ptr(), mask_dev.data_ptr(),
+                     self.aux_dev.data_ptr(), ctx.stream())
 
     def _host(self, dev):
         """Device layout -> reference layout: undo Montgomery (x * 2^-32 mod p,
@@ -652,8 +670,7 @@ class FvBackend(SlotBackend):
                      out3.data_ptr(), scratch.data_ptr(), B, ctx.stream())
             del scratch, a
             out = ctx.empty(B, 2, ctx.k, ctx.n)
-            keyswitch_call(ctx, key.body_dev.data_ptr(), key.mask_dev.data_ptr(),
-                           out3[0, 2].data_ptr(), 3 * stack, out[0, 0].data_ptr(),
+            keyswitch_call(ctx, key, out3[0, 2].data_ptr(), 3 * stack, out[0, 0].data_ptr(),
                            out[0, 1].data_ptr(), 2 * stack, None, out3[0, 0].data_ptr(),
                            out3[0, 1].data_ptr(), 3 * stack, None, None, 0, B)
             res += [out[i] for i in range(B)]
@@ -665,9 +682,8 @@ class FvBackend(SlotBackend):
         ctx = self.ctx
         out = ctx.empty(2, ctx.k, ctx.n)
         key = self.keys.relin
-        keyswitch_call(ctx, key.body_dev.data_ptr(), key.mask_dev.data_ptr(), out3[2].data_ptr(),
-                       0, out[0].data_ptr(), out[1].data_ptr(), 0, None, out3[0].data_ptr(),
-                       out3[1].data_ptr(), 0, None, None, 0, 1)
+        keyswitch_call(ctx, key, out3[2].data_ptr(), 0, out[0].data_ptr(), out[1].data_ptr(), 0,
+                       None, out3[0].data_ptr(), out3[1].data_ptr(), 0, None, None, 0, 1)
         return self._fresh(out, level)
 
     def rotation_hops(self, offset: int) -> list:
@@ -688,9 +704,8 @@ class FvBackend(SlotBackend):
 
         out = ctx.empty(2, ctx.k, ctx.n)
         key = self.keys.galois[off]
-        keyswitch_call(ctx, key.body_dev.data_ptr(), key.mask_dev.data_ptr(), scratch[1].data_ptr(),
-                       0, out[0].data_ptr(), out[1].data_ptr(), 0, None, scratch[0].data_ptr(),
-                       None, 0, None, None, 0, 1)
+        keyswitch_call(ctx, key, scratch[1].data_ptr(), 0, out[0].data_ptr(), out[1].data_ptr(), 0,
+                       None, scratch[0].data_ptr(), None, 0, None, None, 0, 1)
         return out
 
     def _rotate(self, a, offset, level):

@@ -48,23 +48,49 @@ STATS = {"ks_launches": 0, "ks_cts": 0}
 KS_EVENTS = None
 
 
-def keyswitch_call(ctx, *args):
-    """hefv_keyswitch through the context, with the planner's accounting.
-    The batch size is the second-to-last argument."""
+def keyswitch_call(ctx, key, *args):
+    """One batched key switch under ``key`` (a SwitchKey) with the planner's
+    accounting; ``args`` are hefv_keyswitch's after the key pointers (the
+    batch size last).  Keys with an aux-basis form go through
+    hefv_keyswitch_aux (same limbs, fewer transforms)."""
     import torch
 
     batch = int(args[-1])
     STATS["ks_launches"] += 1
     STATS["ks_cts"] += batch
+    if key.aux_dev is not None:
+        scratch, cap = _ks_workspace(ctx, batch)
+        name = "hefv_keyswitch_aux"
+        full = (key.aux_dev.data_ptr(), *args[:-1], scratch.data_ptr(), cap, batch)
+    else:
+        name = "hefv_keyswitch"
+        full = (key.body_dev.data_ptr(), key.mask_dev.data_ptr(), *args)
     if KS_EVENTS is not None:
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        ctx.call("hefv_keyswitch", *args, ctx.stream())
+        ctx.call(name, *full, ctx.stream())
         e1.record()
         KS_EVENTS.append((e0, e1, batch))
     else:
-        ctx.call("hefv_keyswitch", *args, ctx.stream())
+        ctx.call(name, *full, ctx.stream())
+
+
+KS_WORKSPACE_BYTES = 6 << 30
+
+
+def _ks_workspace(ctx, batch: int):
+    """Scratch of the aux-basis key switch (9 k N words per ciphertext),
+    cached on the context; ciphertexts beyond its capacity run in chunks."""
+    import torch
+
+    per_ct = 9 * ctx.k * ctx.n
+    cap = max(1, min(batch, KS_WORKSPACE_BYTES // (4 * per_ct)))
+    ws = getattr(ctx, "_ks_ws", None)
+    if ws is None or ws.numel() < cap * per_ct:
+        ctx._ks_ws = None
+        ws = ctx._ks_ws = torch.empty(cap * per_ct, dtype=torch.int32, device="cuda")
+    return ws, ws.numel() // per_ct
 
 
 def count_layer_ops(rows, x_k: int, s: int, slot_count: int, galois_offsets,
@@ -356,7 +382,7 @@ def _run_rows(backend, rows, x, seg_lists, active, m_arr, off_arr, bias_arr, out
             key = keys[shift]
             g = galois_element(shift, n)
             ctx.call("hefv_automorph", a0, ct_words, None, s0, 2, g, B, st)
-            keyswitch_call(ctx, key.body_dev.data_ptr(), key.mask_dev.data_ptr(), s1, ct_words,
+            keyswitch_call(ctx, key, s1, ct_words,
                            a0, a1, ct_words, None, s0, None, ct_words, a0, a1, ct_words, B)
         # ---- 4. biases and the e0 mask ---------------------------------------------
         bias_rows = [bi for bi, i in enumerate(tile) if bias_arr[i]]
@@ -393,9 +419,8 @@ def _run_rows(backend, rows, x, seg_lists, active, m_arr, off_arr, bias_arr, out
             key = keys[h]
             ctx.call("hefv_automorph", a0, ct_words, d_slot.data_ptr(), b0, 2,
                      galois_element(h, n), nb, st)
-            keyswitch_call(ctx, key.body_dev.data_ptr(), key.mask_dev.data_ptr(),
-                           b0 + stack * 4, ct_words, a0, a1, ct_words, d_slot.data_ptr(), b0, None,
-                           ct_words, None, None, 0, nb)
+            keyswitch_call(ctx, key, b0 + stack * 4, ct_words, a0, a1, ct_words, d_slot.data_ptr(),
+                           b0, None, ct_words, None, None, 0, nb)
         del scr
         # ---- 6. sum pieces into their output ciphertexts -----------------------------
         ms = m_arr[tile]
