@@ -31,6 +31,7 @@
 #include "internal.h"
 #include "kcommon.cuh"
 #include "ntt.cuh"
+#include "tmem.cuh"
 
 namespace hefv {
 
@@ -70,6 +71,10 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 // ---- phase 1: digits -> aux-basis NTTs --------------------------------------
+// CTA = (aux prime t, digit i, KSA_FWD_CTS ciphertexts).  Shoup twiddles of
+// the full passes in shared memory; each digit limb is bulk-copied
+// (cp.async.bulk) into a staging buffer one transform ahead, the copy issued
+// right after the current transform's first CTA barrier.
 template <int LOGN, int LOGE>
 __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
     k_ksa_fwd(const uint32_t* __restrict__ digits, int64_t dig_stride, uint32_t* __restrict__ X,
@@ -83,27 +88,40 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
   extern __shared__ __align__(16) unsigned char smraw[];
   uint2* tws = reinterpret_cast<uint2*>(smraw);
   uint32_t* sm = reinterpret_cast<uint32_t*>(tws + NTW);
+  uint32_t* stage = sm + ((spad_size(N) + 3) & ~3);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(stage + N);
   const int t = blockIdx.x / k;
   const int i = blockIdx.x - t * k;
   const int tid = threadIdx.x;
   const Prime32Info inf = info[aux_base + t];
   const Mod32 md{inf.p, 2 * inf.p};
   const uint2* twg = tw_all + (size_t)(aux_base + t) * N;
+  const int64_t bbeg = (int64_t)blockIdx.y * KSA_FWD_CTS;
+  const int64_t bend = min(B, bbeg + KSA_FWD_CTS);
+  if (tid == 0) {
+    mbar_init(mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   {
     const uint4* src = reinterpret_cast<const uint4*>(twg);
     uint4* dst = reinterpret_cast<uint4*>(tws);
     for (int q = tid; q < NTW / 2; q += NT) dst[q] = __ldg(src + q);
   }
   __syncthreads();
-  const int64_t bbeg = (int64_t)blockIdx.y * KSA_FWD_CTS;
-  const int64_t bend = min(B, bbeg + KSA_FWD_CTS);
+  if (tid == 0) bulk_g2s(stage, digits + bbeg * dig_stride + (size_t)i * N, N * 4, mbar);
+  uint32_t phase = 0;
   for (int64_t b = bbeg; b < bend; ++b) {
-    const uint32_t* src = digits + b * dig_stride + (size_t)i * N;
+    mbar_wait(mbar, phase);
+    phase ^= 1u;
     uint32_t x[E];
     // c_i < p_i < 2^30 <= 4 a_t: a valid lazy input
 #pragma unroll
-    for (int e = 0; e < E; ++e) x[e] = ld_stream(src + tid + e * NT);
-    cta_fwd<LOGN, LOGE, Mod32>(md, x, sm, tws, twg, NoHook(), LOGN - G_::RLAST);
+    for (int e = 0; e < E; ++e) x[e] = stage[tid + e * NT];
+    const uint32_t* nxt = b + 1 < bend ? digits + (b + 1) * dig_stride + (size_t)i * N : nullptr;
+    auto hook = [&]() {
+      if (tid == 0 && nxt) bulk_g2s(stage, nxt, N * 4, mbar);
+    };
+    cta_fwd<LOGN, LOGE, Mod32>(md, x, sm, tws, twg, hook, LOGN - G_::RLAST);
 #pragma unroll
     for (int e = 0; e < E; ++e) x[e] = md.canon4(x[e]);
     store_tiled<LOGN, LOGE>(X + ((size_t)b * 3 + t) * k * (size_t)N, k, i, tid, x);
@@ -214,11 +232,12 @@ __global__ void __launch_bounds__(32 * K, 1)
 }
 
 // ---- phase 3: three inverse NTTs + exact CRT + epilogue ---------------------
-// CTA = (output row jp = part * k + j, KSA_INV_CTS ciphertexts).  The inverse
-// twiddles of the three aux primes' full passes sit in shared memory (the
-// last pass reads its entries through L1); the quotient estimate
-// sum_t y_t / a_t is accumulated as 2^14-scaled fixed point (16 bits per
-// coefficient, error < 3 * 2^-14, far inside the 3/8 rounding margin).
+// CTA = (output row jp = part * k + j, KSA_INV_CTS ciphertexts).  The 3 rows
+// Y[b][t][jp] of each ciphertext stream through a staging buffer by bulk
+// copy, one transform ahead (issued after each transform's first CTA
+// barrier).  The quotient estimate sum_t y_t / a_t is accumulated as
+// 2^14-scaled fixed point (16 bits per coefficient, error < 3 * 2^-14, far
+// inside the 3/8 rounding margin).
 template <int LOGN, int LOGE>
 __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
     k_ksa_inv(const uint32_t* __restrict__ Y, uint32_t* out0, uint32_t* out1, int64_t out_stride,
@@ -231,12 +250,12 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
   constexpr int E = G_::E;
   constexpr int NT = G_::NT;
   constexpr int N = G_::N;
-  constexpr int NTW = 1 << (LOGN - G_::RLAST);
   static_assert(E % 8 == 0, "fixed-point quotient words move 8 at a time");
   extern __shared__ __align__(16) unsigned char smraw[];
-  uint2* tws = reinterpret_cast<uint2*>(smraw);                  // [3][NTW]
-  uint32_t* sm = reinterpret_cast<uint32_t*>(tws + 3 * NTW);
+  uint32_t* sm = reinterpret_cast<uint32_t*>(smraw);
   uint4* vsum = reinterpret_cast<uint4*>(sm + ((spad_size(N) + 3) & ~3));  // [E/8][NT] x 8 u16
+  uint32_t* stage = reinterpret_cast<uint32_t*>(vsum) + N / 2;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(stage + N);
   const int jp = blockIdx.x;
   const int part = jp >= k ? 1 : 0;
   const int j = jp - part * k;
@@ -244,23 +263,31 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
   const Prime32Info pj = info[j];
   const Mod32 mj{pj.p, 2 * pj.p};
   const KsaJ cc = cj[j];
-  for (int t = 0; t < 3; ++t) {
-    const uint4* src = reinterpret_cast<const uint4*>(itw_all + (size_t)(aux_base + t) * N);
-    uint4* dst = reinterpret_cast<uint4*>(tws + t * NTW);
-    for (int q = tid; q < NTW / 2; q += NT) dst[q] = __ldg(src + q);
-  }
-  __syncthreads();
   const int64_t bbeg = (int64_t)blockIdx.y * KSA_INV_CTS;
   const int64_t bend = min(B, bbeg + KSA_INV_CTS);
+  auto row = [&](int64_t b, int t) { return Y + (((size_t)b * 3 + t) * 2 * k + jp) * N; };
+  if (tid == 0) {
+    mbar_init(mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) bulk_g2s(stage, row(bbeg, 0), N * 4, mbar);
+  uint32_t phase = 0;
   for (int64_t b = bbeg; b < bend; ++b) {
     uint32_t acc[E], x[E];
 #pragma unroll 1
     for (int t = 0; t < 3; ++t) {
       const Prime32Info pa = info[aux_base + t];
       const Mod32 ma{pa.p, 2 * pa.p};
-      load_row_vec<LOGN, LOGE>(Y + (((size_t)b * 3 + t) * 2 * k + jp) * N, tid, x);
-      cta_inv<LOGN, LOGE, Mod32>(ma, x, sm, tws + t * NTW, pa.ninv, pa.wn,
-                                 itw_all + (size_t)(aux_base + t) * N);
+      mbar_wait(mbar, phase);
+      phase ^= 1u;
+      load_row_vec<LOGN, LOGE>(stage, tid, x);
+      const uint32_t* nxt = t < 2 ? row(b, t + 1) : (b + 1 < bend ? row(b + 1, 0) : nullptr);
+      auto hook = [&]() {
+        if (tid == 0 && nxt) bulk_g2s(stage, nxt, N * 4, mbar);
+      };
+      cta_inv<LOGN, LOGE, Mod32>(ma, x, sm, itw_all + (size_t)(aux_base + t) * N, pa.ninv, pa.wn,
+                                 nullptr, hook);
       // constant selects (no dynamic indexing of the by-value parameters)
       const uint2 inv = t == 0 ? ct.inv[0] : (t == 1 ? ct.inv[1] : ct.inv[2]);
       const uint2 c = t == 0 ? cc.c[0] : (t == 1 ? cc.c[1] : cc.c[2]);
@@ -292,17 +319,25 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
     for (int q = 0; q < E / 8; ++q) {
       const uint4 vv = vsum[q * NT + tid];
       const uint32_t* vw = reinterpret_cast<const uint32_t*>(&vv);
+      // addends of these 8 coefficients first (all loads in flight; adB may
+      // alias out only at the same index, which this thread alone touches)
+      uint32_t av[8], cv[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int idx = tid + (8 * q + r) * NT;
+        av[r] = a ? __ldg(a + idx) : 0u;
+        cv[r] = c ? c[idx] : 0u;
+      }
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
         const int e = 8 * q + r;
-        const int idx = tid + e * NT;
         const uint32_t f = (r & 1) ? (vw[r >> 1] >> 16) : (vw[r >> 1] & 0xffffu);
         const uint32_t v = ((f + (1u << 13)) >> 14) & 3u;  // rint(sum_t y_t / a_t)
         const uint32_t ev = v == 0 ? cc.e[0] : (v == 1 ? cc.e[1] : (v == 2 ? cc.e[2] : cc.e[3]));
         uint32_t val = mj.canon4(acc[e] + ev);
-        if (a) val = mj.subp(val + a[idx]);
-        if (c) val = mj.subp(val + c[idx]);
-        o[idx] = val;
+        val = mj.subp(val + av[r]);
+        val = mj.subp(val + cv[r]);
+        o[tid + e * NT] = val;
       }
     }
   }
@@ -365,9 +400,9 @@ static int run_ksa(hefv_ctx* c, const uint32_t* kaux, const uint32_t* dig, int64
   auto kf = k_ksa_fwd<LOGN, LE>;
   auto ki = k_ksa_inv<LOGN, LE>;
   const size_t tile = (size_t)((spad_size(G_::N) + 3) & ~3) * 4;
-  const size_t smf = (size_t)(1 << (LOGN - G_::RLAST)) * sizeof(uint2) + tile;
-  const size_t smi = (size_t)3 * (1 << (LOGN - G_::RLAST)) * sizeof(uint2) + tile +
-                     (size_t)G_::N * 2;
+  const size_t smf = (size_t)(1 << (LOGN - G_::RLAST)) * sizeof(uint2) + tile +
+                     (size_t)G_::N * 4 + 16;
+  const size_t smi = tile + (size_t)G_::N * 2 + (size_t)G_::N * 4 + 16;
   HEFV_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smf));
   HEFV_CUDA(cudaFuncSetAttribute(ki, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smi));
   const int64_t chunk = scratch_cts < B ? scratch_cts : B;

@@ -338,11 +338,14 @@ __device__ __forceinline__ void inv_full_pass(const M& md, typename M::T* x, int
 // Exchanges run from fine (warp / group) to coarse (CTA-wide).
 // `itw_last` (optional): table the last pass reads instead of `itw` (e.g. the
 // full-pass entries staged in shared memory as `itw`, the rest from global).
-template <int LOGN, int LOGE, class M>
+// `hook` runs right after the transform's first CTA-wide barrier (every
+// thread has consumed its input registers' source by then).
+template <int LOGN, int LOGE, class M, class Hook = NoHook>
 __device__ __forceinline__ void cta_inv(const M& md, typename M::T* x, typename M::T* sm,
                                         const typename M::Tw* __restrict__ itw,
                                         typename M::Tw ninv, typename M::Tw wn,
-                                        const typename M::Tw* __restrict__ itw_last = nullptr) {
+                                        const typename M::Tw* __restrict__ itw_last = nullptr,
+                                        const Hook& hook = Hook()) {
   typedef Geo<LOGN, LOGE> G_;
   constexpr int LOG_NT = LOGN - LOGE;
   const int tid = threadIdx.x;
@@ -354,6 +357,7 @@ __device__ __forceinline__ void cta_inv(const M& md, typename M::T* x, typename 
     const int K = xpad_k(LOGN, LOGE, pass), S = xpad_s(LOGN, LOGE, pass);
     if (pass == G_::NFULL - 1) {
       __syncthreads();  // the tile may still be in use by a previous transform
+      hook();
 #pragma unroll
       for (int e = 0; e < G_::E; ++e) sm[xaddr_row<LOGN, LOGE>(tid, e, K, S)] = x[e];
     } else {
