@@ -8,7 +8,8 @@
 //   kind 3: IADD3     (ALU pipe reference)
 //   kind 4: one lazy Shoup Cooley-Tukey butterfly (counted as 1 op)
 //   kind 5: one lazy 64-bit Shoup butterfly (p < 2^62; counted as 1 op)
-//   kind 6: IMAD.WIDE.U32 multiply-accumulate into 64 bits (mad.wide.u32)
+//   kind 6: mad.wide.u32 into a 64-bit running sum whose bits feed the next
+//           multiplier (a dependent chain: the product cannot be hoisted)
 //   kind 7: DFMA (fp64 fused multiply-add)
 // Each thread runs 8 independent chains so the pipes, not latency, bound it.
 #include "../../include/hefv.h"
@@ -98,8 +99,11 @@ __global__ void __launch_bounds__(256) k_probe_madwide(uint32_t* out, int iters,
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-        asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc[i]) : "r"(a[i]), "r"(b));
+      for (int i = 0; i < 8; ++i) {
+        // multiplier taken from the running sum: no product can be hoisted
+        const uint32_t m = (uint32_t)(acc[i] >> 7) | b;
+        asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc[i]) : "r"(a[i]), "r"(m));
+      }
     }
   }
   uint64_t s = 0;
