@@ -266,6 +266,8 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
   const int64_t bbeg = (int64_t)blockIdx.y * KSA_INV_CTS;
   const int64_t bend = min(B, bbeg + KSA_INV_CTS);
   auto row = [&](int64_t b, int t) { return Y + (((size_t)b * 3 + t) * 2 * k + jp) * N; };
+  __shared__ Prime32Info ainfo[3];  // the aux primes' constants, read every transform
+  if (tid < 3) ainfo[tid] = info[aux_base + tid];
   if (tid == 0) {
     mbar_init(mbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -277,7 +279,7 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
     uint32_t acc[E], x[E];
 #pragma unroll 1
     for (int t = 0; t < 3; ++t) {
-      const Prime32Info pa = info[aux_base + t];
+      const Prime32Info pa = ainfo[t];
       const Mod32 ma{pa.p, 2 * pa.p};
       mbar_wait(mbar, phase);
       phase ^= 1u;
