@@ -131,101 +131,163 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
 // ---- phase 2: per-point contraction over digits ----------------------------
 // CTA = (aux prime t, 32-point tile m); warp w = target prime j, lane =
 // point.  Each thread keeps its point's body and mask key words of every
-// digit in registers (2K words); the CTA streams the ciphertexts' digit tiles
-// (k x 32 words, one word per thread) through a KSA_STAGES-deep cp.async
-// ring in shared memory, and every tile word feeds two 64-bit multiply-adds.
+// digit in registers (2K words).
 constexpr int KSA_STAGES = 4;
 
 __device__ __forceinline__ void mad_wide(uint64_t& acc, uint32_t a, uint32_t b) {
   asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc) : "r"(a), "r"(b));
 }
 
-// s mod a for s < 2^62 with 32-bit operations: s = hi 2^32 + lo,
-// hi 2^32 = hi * R (R = 2^32 mod a, Shoup), lo by a 32-bit Barrett step.
-struct Red64 {
-  uint32_t a, r, rsh, mu;  // a; 2^32 mod a; floor(R 2^32 / a); floor(2^32 / a)
+__device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(mbar);
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+
+// Montgomery reduction of s < 2^61: s 2^-32 mod a, canonical.
+// (s + m a) / 2^32 < 2^29 + a < 4a for a > 2^28.
+struct Redc {
+  uint32_t a, nainv;  // -a^-1 mod 2^32
   __device__ __forceinline__ uint32_t operator()(uint64_t s) const {
-    const uint32_t hi = (uint32_t)(s >> 32), lo = (uint32_t)s;
-    const uint32_t h = Mod32::mul_shoup(hi, r, rsh, a);          // [0, 2a)
-    const uint32_t q = __umulhi(lo, mu);
-    const uint32_t l = lo - q * a;                               // [0, 2a)
-    uint32_t v = h + l;                                          // [0, 4a)
+    const uint32_t m = (uint32_t)s * nainv;
+    mad_wide(s, m, a);
+    uint32_t v = (uint32_t)(s >> 32);
     v = min(v, v - 2 * a);
     return min(v, v - a);
   }
 };
 
-// K: digits contracted per point (compile time; rows k..K-1 of the ring hold
-// stale words and meet zero key words).
+// Phase-2 contraction, Winograd's inner product over digit pairs u = (2u, 2u+1):
+//   sum_i x_i k_i = sum_u (x_2u + k_2u+1)(x_2u+1 + k_2u)
+//                   - sum_u x_2u x_2u+1 - sum_u k_2u k_2u+1.
+// The x-pair sum is shared by all 2k outputs of a point (one warp computes it
+// per ciphertext), the k-pair sums are per-thread constants, and both factor
+// sums of a pair come from ONE 64-bit add of the packed words (x_2u+1 : x_2u)
+// + (k_2u : k_2u+1) (no carry crosses: x + k < 2^29.25).  Half the 64-bit
+// multiplies of the direct sum.  Bounds: each of the two accumulation chains
+// sums <= 6 products < 2^58.5, so everything stays below 2^62 and the
+// difference is the exact dot product (< k a^2 < 2^61).  The output is
+// Montgomery-reduced (x 2^-32, undone by phase 3's CRT constant).
+//
+// K: digits per point (compile time, even; ring rows k..K-1 are zeroed once
+// and their key words are zero, so padded pairs contribute nothing).
+// Warps 0..K-1 consume (warp w = target prime j when w < k), warp K computes
+// the x-pair sums, warp K+1 streams each ciphertext's k x 32-word digit tile
+// with one bulk copy into a KSA_STAGES-deep ring (full / xready / empty
+// mbarriers, no CTA-wide barrier in the loop).
 template <int K>
-__global__ void __launch_bounds__(32 * K, 1)
+__global__ void __launch_bounds__(32 * (K + 2), 1)
     k_ksa_mac(const uint32_t* __restrict__ X, const uint32_t* __restrict__ kaux,
               uint32_t* __restrict__ Y, int64_t B, int k, int log_n, int aux_base,
               const Prime32Info* __restrict__ info) {
-  __shared__ __align__(16) uint32_t ring[KSA_STAGES][K * 32];
+  static_assert(K % 2 == 0, "digit pairs");
+  constexpr int H = K / 2;
+  __shared__ __align__(128) uint32_t ring[KSA_STAGES][K * 32];
+  __shared__ __align__(16) uint64_t xpair[KSA_STAGES][32];
+  __shared__ __align__(8) uint64_t full[KSA_STAGES], xready[KSA_STAGES], empty[KSA_STAGES];
   const int n = 1 << log_n;
   const int tiles = n >> 5;
   const int t = blockIdx.x / tiles;
   const int m = blockIdx.x - t * tiles;
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
-  const bool active = w < k;
-  const int j = active ? w : 0;
-  const uint32_t a = info[aux_base + t].p;
-  Red64 red;
-  red.a = a;
-  red.r = (uint32_t)((1ull << 32) % a);
-  red.rsh = (uint32_t)(((uint64_t)red.r << 32) / a);
-  red.mu = (uint32_t)((1ull << 32) / a);
-  uint32_t kb[K], km[K];
-  const size_t kstride = (size_t)k * k * n;  // body -> mask rows of the same t
-  const uint32_t* ks = kaux + (((size_t)t * 2 * k + j) * tiles + m) * k * 32 + lane;
-#pragma unroll
-  for (int i = 0; i < K; ++i) {
-    kb[i] = i < k ? __ldg(ks + 32 * i) : 0u;
-    km[i] = i < k ? __ldg(ks + kstride + 32 * i) : 0u;
-  }
   const int64_t bbeg = (int64_t)blockIdx.y * KSA_MAC_CTS;
   const int64_t bend = min(B, bbeg + KSA_MAC_CTS);
   const int nb = (int)(bend - bbeg);
-  const bool copier = threadIdx.x < k * 32;
+  const uint32_t tile_bytes = (uint32_t)k * 32 * 4;
   // X tile of ciphertext b: (((b * 3 + t) * tiles + m) * k) * 32 words, k*32 long
   const size_t xstride = (size_t)3 * tiles * k * 32;
-  const uint32_t* xsrc = X + (((size_t)bbeg * 3 + t) * tiles + m) * k * 32 + threadIdx.x;
-#pragma unroll
-  for (int s = 0; s < KSA_STAGES - 1; ++s) {
-    if (copier && s < nb) cp_async4(&ring[s][threadIdx.x], xsrc + s * xstride);
-    cp_async_commit();
+  const uint32_t* xsrc = X + (((size_t)bbeg * 3 + t) * tiles + m) * k * 32;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < KSA_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&xready[s], 1);
+      mbar_init(&empty[s], K + 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  xsrc += (KSA_STAGES - 1) * xstride;
+  for (int q = k * 32 + threadIdx.x; q < K * 32; q += blockDim.x)
+    for (int s = 0; s < KSA_STAGES; ++s) ring[s][q] = 0u;
+  __syncthreads();
+  if (w == K + 1) {  // producer
+    if (lane == 0) {
+      for (int r = 0; r < nb; ++r) {
+        const int s = r % KSA_STAGES;
+        if (r >= KSA_STAGES) mbar_wait(&empty[s], (uint32_t)((r / KSA_STAGES - 1) & 1));
+        bulk_g2s(ring[s], xsrc + (size_t)r * xstride, tile_bytes, &full[s]);
+      }
+    }
+    return;
+  }
+  if (w == K) {  // x-pair sums
+    for (int r = 0; r < nb; ++r) {
+      const int s = r % KSA_STAGES;
+      mbar_wait(&full[s], (uint32_t)((r / KSA_STAGES) & 1));
+      const uint32_t* xt = ring[s] + lane;
+      uint64_t p0 = 0, p1 = 0;
+#pragma unroll
+      for (int u = 0; u < H; ++u) mad_wide((u & 1) ? p1 : p0, xt[64 * u], xt[64 * u + 32]);
+      xpair[s][lane] = p0 + p1;
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&xready[s]);
+        mbar_arrive(&empty[s]);
+      }
+    }
+    return;
+  }
+  const bool active = w < k;
+  const int j = active ? w : 0;
+  Redc red;
+  red.a = info[aux_base + t].p;
+  {
+    uint32_t inv = red.a;  // a^-1 mod 2^32 by Newton (a odd)
+#pragma unroll
+    for (int it = 0; it < 5; ++it) inv *= 2u - red.a * inv;
+    red.nainv = 0u - inv;
+  }
+  // packed key pairs (k_2u : k_2u+1) of body and mask, and their pair sums
+  uint64_t kb[H], km[H];
+  uint64_t kpb = 0, kpm = 0;
+  {
+    const size_t kstride = (size_t)k * k * n;  // body -> mask rows of the same t
+    const uint32_t* ks = kaux + (((size_t)t * 2 * k + j) * tiles + m) * k * 32 + lane;
+#pragma unroll
+    for (int u = 0; u < H; ++u) {
+      const int i0 = 2 * u, i1 = 2 * u + 1;
+      const uint32_t b0 = i0 < k ? __ldg(ks + 32 * i0) : 0u;
+      const uint32_t b1 = i1 < k ? __ldg(ks + 32 * i1) : 0u;
+      const uint32_t m0 = i0 < k ? __ldg(ks + kstride + 32 * i0) : 0u;
+      const uint32_t m1 = i1 < k ? __ldg(ks + kstride + 32 * i1) : 0u;
+      kb[u] = ((uint64_t)b0 << 32) | b1;
+      km[u] = ((uint64_t)m0 << 32) | m1;
+      mad_wide(kpb, b0, b1);
+      mad_wide(kpm, m0, m1);
+    }
+  }
   uint32_t* yb = Y + (((size_t)bbeg * 3 + t) * 2 * k + j) * (size_t)n + (m << 5) + lane;
   const size_t ymask = (size_t)k * n;
   const size_t ystride = (size_t)3 * 2 * k * n;
   for (int r = 0; r < nb; ++r) {
-    cp_async_wait<KSA_STAGES - 2>();
-    __syncthreads();  // tile r visible to all; slot (r - 1) % S free for reuse
-    if (copier && r + KSA_STAGES - 1 < nb)
-      cp_async4(&ring[(r + KSA_STAGES - 1) % KSA_STAGES][threadIdx.x], xsrc);
-    cp_async_commit();
-    xsrc += xstride;
-    const uint32_t* xt = ring[r % KSA_STAGES] + lane;
+    const int s = r % KSA_STAGES;
+    const uint32_t ph = (uint32_t)((r / KSA_STAGES) & 1);
+    mbar_wait(&full[s], ph);
+    const uint32_t* xt = ring[s] + lane;
     uint64_t b0 = 0, b1 = 0, m0 = 0, m1 = 0;
 #pragma unroll
-    for (int i = 0; i + 1 < K; i += 2) {
-      const uint32_t x0 = xt[32 * i], x1 = xt[32 * (i + 1)];
-      mad_wide(b0, x0, kb[i]);
-      mad_wide(m0, x0, km[i]);
-      mad_wide(b1, x1, kb[i + 1]);
-      mad_wide(m1, x1, km[i + 1]);
+    for (int u = 0; u < H; ++u) {
+      // (x_2u+1 : x_2u) + (k_2u : k_2u+1) = (x_2u+1 + k_2u : x_2u + k_2u+1)
+      const uint64_t xx = ((uint64_t)xt[64 * u + 32] << 32) | xt[64 * u];
+      const uint64_t sb = xx + kb[u], sm = xx + km[u];
+      mad_wide((u & 1) ? b1 : b0, (uint32_t)sb, (uint32_t)(sb >> 32));
+      mad_wide((u & 1) ? m1 : m0, (uint32_t)sm, (uint32_t)(sm >> 32));
     }
-    if constexpr (K & 1) {
-      const uint32_t x0 = xt[32 * (K - 1)];
-      mad_wide(b0, x0, kb[K - 1]);
-      mad_wide(m0, x0, km[K - 1]);
-    }
+    mbar_wait(&xready[s], ph);
+    const uint64_t xp = xpair[s][lane];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
     if (active) {
-      yb[0] = red(b0 + b1);
-      yb[ymask] = red(m0 + m1);
+      yb[0] = red(b0 + b1 - xp - kpb);
+      yb[ymask] = red(m0 + m1 - xp - kpm);
     }
     yb += ystride;
   }
@@ -420,12 +482,12 @@ static int run_ksa(hefv_ctx* c, const uint32_t* kaux, const uint32_t* dig, int64
     {
       dim3 grid((unsigned)(3 * (n >> 5)), (unsigned)((nb + KSA_MAC_CTS - 1) / KSA_MAC_CTS));
       if (k == 22)
-        k_ksa_mac<22><<<grid, 32 * 22, 0, st>>>(X, kaux, Y, nb, k, c->log_n, ab, c->d_info32);
+        k_ksa_mac<22><<<grid, 32 * 24, 0, st>>>(X, kaux, Y, nb, k, c->log_n, ab, c->d_info32);
       else if (k <= 16)
-        k_ksa_mac<16><<<grid, 32 * 16, 0, st>>>(X, kaux, Y, nb, k, c->log_n, ab, c->d_info32);
+        k_ksa_mac<16><<<grid, 32 * 18, 0, st>>>(X, kaux, Y, nb, k, c->log_n, ab, c->d_info32);
       else
-        k_ksa_mac<KSA_KMAX><<<grid, 32 * KSA_KMAX, 0, st>>>(X, kaux, Y, nb, k, c->log_n, ab,
-                                                             c->d_info32);
+        k_ksa_mac<KSA_KMAX><<<grid, 32 * (KSA_KMAX + 2), 0, st>>>(X, kaux, Y, nb, k, c->log_n,
+                                                                   ab, c->d_info32);
       HEFV_LAUNCH_CHECK("k_ksa_mac");
     }
     {
@@ -527,7 +589,9 @@ int hefv_ks_aux_setup(hefv_ctx* c, int32_t aux_base) {
   for (int t = 0; t < 3; ++t) {
     const uint32_t u = a[(t + 1) % 3], v = a[(t + 2) % 3];
     const uint64_t rest = mulmod_u64(u, v, a[t]);
-    ct.inv[t] = shoup_pair((uint32_t)powmod_u64(rest, a[t] - 2, a[t]), a[t]);
+    // phase 2 outputs Y 2^-32 (Montgomery reduction): fold 2^32 back in here
+    const uint64_t inv_t = powmod_u64(rest, a[t] - 2, a[t]);
+    ct.inv[t] = shoup_pair((uint32_t)mulmod_u64(inv_t, (1ull << 32) % a[t], a[t]), a[t]);
     ct.qs[t] = (uint32_t)((1ull << 46) / a[t]);
   }
   std::vector<KsaJ> cj(k);
