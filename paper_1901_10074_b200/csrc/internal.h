@@ -15,7 +15,8 @@ struct KsaJ {
   uint32_t e[4];   // (-v A) mod p_j, v = 0..3
 };
 struct KsaT {
-  uint2 inv[3];    // (A / a_t)^-1 mod a_t, Shoup pair
+  uint2 ninv[3];   // N^-1 (A / a_t)^-1 2^32 mod a_t, Shoup pair (last inverse stage)
+  uint2 wn[3];     // psi_rev^-1[1] N^-1 (A / a_t)^-1 2^32 mod a_t, Shoup pair
   uint32_t qs[3];  // floor(2^46 / a_t): y * 2^14 / a_t = umulhi(y, qs)
 };
 }  // namespace hefv

@@ -16,8 +16,9 @@
 //
 //   phase 1  k_ksa_fwd : X[b][t][i]    = NTT_{a_t}(c_i)                (device order)
 //   phase 2  k_ksa_mac : Y[b][t][jp]   = sum_i X[b][t][i] * Kaux[t][jp][i]   mod a_t
-//   phase 3  k_ksa_inv : r_t = iNTT_{a_t}(Y[b][t][jp]);  exact CRT over t:
-//            y_t = r_t (A/a_t)^-1 mod a_t,  v = rint(sum_t y_t / a_t),
+//   phase 3  k_ksa_inv : y_t = iNTT_{a_t}(Y[b][t][jp]) (A/a_t)^-1 mod a_t (the
+//            factor rides on the last stage's N^-1);  exact CRT over t:
+//            v = rint(sum_t y_t / a_t),
 //            d = sum_t y_t (A/a_t) - v A   (the centred integer),  out = d mod p_j
 //            + the caller's epilogue addends.
 // v is exact from a 2^-14 fixed-point sum because |d| / A < 2^-3: the
@@ -39,11 +40,6 @@ constexpr int KSA_FWD_CTS = 8;   // ciphertexts per CTA, phase 1
 constexpr int KSA_INV_CTS = 8;   // ciphertexts per CTA, phase 3
 constexpr int KSA_MAC_CTS = 128;  // ciphertexts per CTA, phase 2 (key tile reuse)
 constexpr int KSA_KMAX = 24;     // digits held in registers by phase 2
-
-__device__ __forceinline__ uint32_t shoup_canon(uint32_t x, uint2 w, uint32_t p) {
-  const uint32_t r = Mod32::mul_shoup(x, w.x, w.y, p);
-  return r >= p ? r - p : r;
-}
 
 // "Tiled" point layout of a (k, N) stack: [N/32][k][32] -- the k values of a
 // 32-point tile are one contiguous 128k-byte block, which phase 2 streams
@@ -350,10 +346,13 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
       auto hook = [&]() {
         if (tid == 0 && nxt) bulk_g2s(stage, nxt, N * 4, mbar);
       };
-      cta_inv<LOGN, LOGE, Mod32>(ma, x, sm, itw_all + (size_t)(aux_base + t) * N, pa.ninv, pa.wn,
-                                 nullptr, hook);
       // constant selects (no dynamic indexing of the by-value parameters)
-      const uint2 inv = t == 0 ? ct.inv[0] : (t == 1 ? ct.inv[1] : ct.inv[2]);
+      const uint2 ninv = t == 0 ? ct.ninv[0] : (t == 1 ? ct.ninv[1] : ct.ninv[2]);
+      const uint2 wn = t == 0 ? ct.wn[0] : (t == 1 ? ct.wn[1] : ct.wn[2]);
+      // the last inverse stage's N^-1 carries the CRT factor (A/a_t)^-1 2^32:
+      // the transform's output is y_t directly
+      cta_inv<LOGN, LOGE, Mod32>(ma, x, sm, itw_all + (size_t)(aux_base + t) * N, ninv, wn,
+                                 nullptr, hook);
       const uint2 c = t == 0 ? cc.c[0] : (t == 1 ? cc.c[1] : cc.c[2]);
       const uint32_t qs = t == 0 ? ct.qs[0] : (t == 1 ? ct.qs[1] : ct.qs[2]);
 #pragma unroll
@@ -363,7 +362,7 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
           const int e = 8 * q + r;
-          const uint32_t y = shoup_canon(ma.subp(x[e]), inv, pa.p);
+          const uint32_t y = ma.subp(x[e]);
           // y * 2^14 / a_t, rounded down (< 2^14): 16-bit lanes never carry
           const uint32_t f = __umulhi(y, qs);
           vw[r >> 1] += (r & 1) ? (f << 16) : f;
@@ -589,9 +588,13 @@ int hefv_ks_aux_setup(hefv_ctx* c, int32_t aux_base) {
   for (int t = 0; t < 3; ++t) {
     const uint32_t u = a[(t + 1) % 3], v = a[(t + 2) % 3];
     const uint64_t rest = mulmod_u64(u, v, a[t]);
-    // phase 2 outputs Y 2^-32 (Montgomery reduction): fold 2^32 back in here
-    const uint64_t inv_t = powmod_u64(rest, a[t] - 2, a[t]);
-    ct.inv[t] = shoup_pair((uint32_t)mulmod_u64(inv_t, (1ull << 32) % a[t], a[t]), a[t]);
+    // phase 2 outputs Y 2^-32 (Montgomery reduction): fold 2^32 back in here,
+    // and fold the whole factor into the last inverse stage (N^-1 and
+    // psi^-1 N^-1 of that stage are multiplied by it)
+    const uint64_t inv_t = mulmod_u64(powmod_u64(rest, a[t] - 2, a[t]), (1ull << 32) % a[t], a[t]);
+    const Prime32Info& ia = c->info32[aux_base + t];
+    ct.ninv[t] = shoup_pair((uint32_t)mulmod_u64(ia.ninv.x, inv_t, a[t]), a[t]);
+    ct.wn[t] = shoup_pair((uint32_t)mulmod_u64(ia.wn.x, inv_t, a[t]), a[t]);
     ct.qs[t] = (uint32_t)((1ull << 46) / a[t]);
   }
   std::vector<KsaJ> cj(k);
