@@ -70,7 +70,8 @@ def _both(params, B, seed, extremes=False):
     return outs
 
 
-@pytest.mark.parametrize("logn,k,B", [(14, 22, 9), (14, 24, 5), (13, 12, 7), (10, 9, 11)])
+@pytest.mark.parametrize("logn,k,B", [(14, 22, 9), (14, 24, 5), (13, 12, 7), (12, 17, 6), (11, 16, 5),
+                                      (10, 9, 11)])
 def test_aux_keyswitch_equals_per_prime(logn, k, B):
     direct, aux = _both(_params(logn, k), B, seed=logn * 100 + k, extremes=True)
     assert np.array_equal(direct, aux)
