@@ -27,6 +27,7 @@
 // Kaux[t][part*k + j][i] = NTT_{a_t}(B_ji) (body part 0, mask part 1) is built
 // once per switch key by hefv_ks_aux_key.
 #include <cmath>
+#include <cstdlib>
 
 #include "../../include/hefv.h"
 #include "internal.h"
@@ -449,23 +450,57 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
   }
 }
 
+template <int LOGN, int LF, int LI>
+static int run_ksa_e(hefv_ctx* c, const uint32_t* kaux, const uint32_t* dig, int64_t ds,
+                     uint32_t* o0, uint32_t* o1, int64_t os, const int32_t* slot,
+                     const uint32_t* a0, const uint32_t* a1, int64_t as, const uint32_t* b0,
+                     const uint32_t* b1, int64_t bs, uint32_t* scratch, int64_t scratch_cts,
+                     int64_t B, cudaStream_t st);
+
 template <int LOGN>
 static int run_ksa(hefv_ctx* c, const uint32_t* kaux, const uint32_t* dig, int64_t ds,
                    uint32_t* o0, uint32_t* o1, int64_t os, const int32_t* slot,
                    const uint32_t* a0, const uint32_t* a1, int64_t as, const uint32_t* b0,
                    const uint32_t* b1, int64_t bs, uint32_t* scratch, int64_t scratch_cts,
                    int64_t B, cudaStream_t st) {
-  constexpr int LE = 4;
-  typedef Geo<LOGN, LE> G_;
+  // transform geometry: 16 words per thread by default; HEFV_KSA_E32 = 1 / 2
+  // / 3 selects 32 words per thread (512 threads) for fwd / inv / both at 2^14
+  if constexpr (LOGN == 14) {
+    static const int e32 = [] {
+      const char* v = getenv("HEFV_KSA_E32");
+      return v ? atoi(v) : 0;
+    }();
+    if (e32 == 1)
+      return run_ksa_e<LOGN, 5, 4>(c, kaux, dig, ds, o0, o1, os, slot, a0, a1, as, b0, b1, bs,
+                                   scratch, scratch_cts, B, st);
+    if (e32 == 2)
+      return run_ksa_e<LOGN, 4, 5>(c, kaux, dig, ds, o0, o1, os, slot, a0, a1, as, b0, b1, bs,
+                                   scratch, scratch_cts, B, st);
+    if (e32 == 3)
+      return run_ksa_e<LOGN, 5, 5>(c, kaux, dig, ds, o0, o1, os, slot, a0, a1, as, b0, b1, bs,
+                                   scratch, scratch_cts, B, st);
+  }
+  return run_ksa_e<LOGN, 4, 4>(c, kaux, dig, ds, o0, o1, os, slot, a0, a1, as, b0, b1, bs,
+                               scratch, scratch_cts, B, st);
+}
+
+template <int LOGN, int LF, int LI>
+static int run_ksa_e(hefv_ctx* c, const uint32_t* kaux, const uint32_t* dig, int64_t ds,
+                     uint32_t* o0, uint32_t* o1, int64_t os, const int32_t* slot,
+                     const uint32_t* a0, const uint32_t* a1, int64_t as, const uint32_t* b0,
+                     const uint32_t* b1, int64_t bs, uint32_t* scratch, int64_t scratch_cts,
+                     int64_t B, cudaStream_t st) {
+  typedef Geo<LOGN, LF> GF;
+  typedef Geo<LOGN, LI> GI;
   const int k = c->k;
   const int64_t n = c->n;
   const int ab = c->ksa_base;
-  auto kf = k_ksa_fwd<LOGN, LE>;
-  auto ki = k_ksa_inv<LOGN, LE>;
-  const size_t tile = (size_t)((spad_size(G_::N) + 3) & ~3) * 4;
-  const size_t smf = (size_t)(1 << (LOGN - G_::RLAST)) * sizeof(uint2) + tile +
-                     (size_t)G_::N * 4 + 16;
-  const size_t smi = tile + (size_t)G_::N * 2 + (size_t)G_::N * 4 + 16;
+  auto kf = k_ksa_fwd<LOGN, LF>;
+  auto ki = k_ksa_inv<LOGN, LI>;
+  const size_t tile = (size_t)((spad_size(GF::N) + 3) & ~3) * 4;
+  const size_t smf = (size_t)(1 << (LOGN - GF::RLAST)) * sizeof(uint2) + tile +
+                     (size_t)GF::N * 4 + 16;
+  const size_t smi = tile + (size_t)GI::N * 2 + (size_t)GI::N * 4 + 16;
   HEFV_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smf));
   HEFV_CUDA(cudaFuncSetAttribute(ki, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smi));
   const int64_t chunk = scratch_cts < B ? scratch_cts : B;
@@ -475,7 +510,7 @@ static int run_ksa(hefv_ctx* c, const uint32_t* kaux, const uint32_t* dig, int64
     const int64_t nb = (B - c0) < chunk ? (B - c0) : chunk;
     {
       dim3 grid((unsigned)(3 * k), (unsigned)((nb + KSA_FWD_CTS - 1) / KSA_FWD_CTS));
-      kf<<<grid, G_::NT, smf, st>>>(dig + c0 * ds, ds, X, nb, k, ab, c->d_tw32, c->d_info32);
+      kf<<<grid, GF::NT, smf, st>>>(dig + c0 * ds, ds, X, nb, k, ab, c->d_tw32, c->d_info32);
       HEFV_LAUNCH_CHECK("k_ksa_fwd");
     }
     {
@@ -502,7 +537,7 @@ static int run_ksa(hefv_ctx* c, const uint32_t* kaux, const uint32_t* dig, int64
         if (bb0) bb0 += c0 * bs;
         if (bb1) bb1 += c0 * bs;
       }
-      ki<<<grid, G_::NT, smi, st>>>(Y, oo0, oo1, os, sl, a0 ? a0 + c0 * as : nullptr,
+      ki<<<grid, GI::NT, smi, st>>>(Y, oo0, oo1, os, sl, a0 ? a0 + c0 * as : nullptr,
                                     a1 ? a1 + c0 * as : nullptr, as, bb0, bb1, bs, nb, k, ab,
                                     c->d_itw32, c->d_info32, c->d_ksa_j, c->ksa_t);
       HEFV_LAUNCH_CHECK("k_ksa_inv");
