@@ -76,7 +76,7 @@ def keyswitch_call(ctx, key, *args):
         ctx.call(name, *full, ctx.stream())
 
 
-KS_WORKSPACE_BYTES = 6 << 30
+KS_WORKSPACE_BYTES = 16 << 30  # ~1300 ciphertexts per chunk at retina (fewer kernel tails)
 
 
 def _ks_workspace(ctx, batch: int):

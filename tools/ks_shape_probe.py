@@ -36,7 +36,9 @@ s1 = s0 + stack * 4
 ws = None
 if key.aux_dev is not None:
     per_ct = 9 * k * n
-    cap = max(1, min(B, (6 << 30) // (4 * per_ct)))
+    import os
+
+    cap = max(1, min(B, int(float(os.environ.get("KS_WS_GB", "6")) * (1 << 30)) // (4 * per_ct)))
     ws = torch.empty(cap * per_ct, dtype=torch.int32, device="cuda")
 
 
