@@ -1,3 +1,8 @@
+"""cProfile of one config-2 encrypted inference on the GPU (host-side view:
+how much of the step the host spends outside the blocking launches).
+
+python tools/prof_infer.py
+"""
 import cProfile, pstats, sys, time
 sys.path.insert(0, ".")
 import numpy as np, torch
