@@ -37,9 +37,18 @@
 
 namespace hefv {
 
-constexpr int KSA_FWD_CTS = 8;   // ciphertexts per CTA, phase 1
-constexpr int KSA_INV_CTS = 8;   // ciphertexts per CTA, phase 3
-constexpr int KSA_MAC_CTS = 128;  // ciphertexts per CTA, phase 2 (key tile reuse)
+#ifndef KSA_FWD_CTS_V
+#define KSA_FWD_CTS_V 8
+#endif
+#ifndef KSA_INV_CTS_V
+#define KSA_INV_CTS_V 8
+#endif
+#ifndef KSA_MAC_CTS_V
+#define KSA_MAC_CTS_V 128
+#endif
+constexpr int KSA_FWD_CTS = KSA_FWD_CTS_V;  // ciphertexts per CTA, phase 1
+constexpr int KSA_INV_CTS = KSA_INV_CTS_V;  // ciphertexts per CTA, phase 3
+constexpr int KSA_MAC_CTS = KSA_MAC_CTS_V;  // ciphertexts per CTA, phase 2 (key tile reuse)
 constexpr int KSA_KMAX = 24;     // digits held in registers by phase 2
 
 // "Tiled" point layout of a (k, N) stack: [N/32][k][32] -- the k values of a
