@@ -10,6 +10,7 @@
 #include "internal.h"
 #include "ntt.cuh"
 #include "kcommon.cuh"
+#include "tmem.cuh"
 
 namespace hefv {
 
@@ -83,6 +84,125 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT)
   for (int e = 0; e < G_::E; ++e) dst[tid + e * G_::NT] = md.subp(x[e]);
 }
 
+// ---- batched device-order path for 32-bit primes, N >= 2^10 ---------------
+// Persistent: one wave of CTAs (as many per SM as fit), CTA c owns the range
+// [c P / G, (c+1) P / G) of the P = batch x nprimes polynomials in prime-major
+// order, so every SM gets the same number of transforms (no partial last
+// wave) and restages twiddles only at a prime boundary.  The prime's Shoup
+// twiddles of the full passes live in shared memory; each polynomial is
+// bulk-copied (cp.async.bulk) into a staging buffer one transform ahead (the
+// copy is issued right after the current transform's first CTA barrier).
+
+// x < 2^32 -> [0, 4p), the lazy forward transform's input range
+__device__ __forceinline__ uint32_t to_lazy4(uint32_t x, const Prime32Info& inf) {
+  if (inf.p >= (1u << 30)) return x;
+  if (inf.p > (1u << 29)) return x >= 4 * inf.p ? x - 4 * inf.p : x;
+  return barrett62(x, inf.p, inf.mu);
+}
+
+template <int LOGN, bool FWD>
+__global__ void __launch_bounds__(Geo<LOGN, 4>::NT, 1024 / Geo<LOGN, 4>::NT)
+    k_ntt32_b(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int64_t batch,
+              int nprimes, int prime_base, const uint2* __restrict__ tw_all,
+              const Prime32Info* __restrict__ info) {
+  typedef Geo<LOGN, 4> G_;
+  constexpr int E = G_::E;
+  constexpr int NT = G_::NT;
+  constexpr int N = G_::N;
+  constexpr int NTW = 1 << (LOGN - G_::RLAST);
+  extern __shared__ __align__(16) unsigned char smraw[];
+  uint2* tws = reinterpret_cast<uint2*>(smraw);
+  uint32_t* sm = reinterpret_cast<uint32_t*>(tws + NTW);
+  uint32_t* stage = sm + ((spad_size(N) + 3) & ~3);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(stage + N);
+  const int tid = threadIdx.x;
+  const int64_t P = batch * nprimes;
+  const int64_t qbeg = P * blockIdx.x / gridDim.x;
+  const int64_t qend = P * (blockIdx.x + 1) / gridDim.x;
+  if (qbeg >= qend) return;
+  // prime-major work order q -> (prime j, batch index b); memory is (b, j, N)
+  auto poly = [&](int64_t q) {
+    const int64_t j = q / batch, b = q - j * batch;
+    return (b * nprimes + j) * (int64_t)N;
+  };
+  if (tid == 0) {
+    mbar_init(mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) bulk_g2s(stage, in + poly(qbeg), N * 4, mbar);
+  uint32_t phase = 0;
+  int cur = -1;
+  Prime32Info inf;
+  const uint2* twg = nullptr;
+  for (int64_t q = qbeg; q < qend; ++q) {
+    const int j = (int)(q / batch);
+    if (j != cur) {  // (re)stage this prime's full-pass twiddles
+      cur = j;
+      inf = info[prime_base + j];
+      twg = tw_all + (size_t)(prime_base + j) * N;
+      __syncthreads();  // the previous prime's table is no longer read
+      const uint4* src = reinterpret_cast<const uint4*>(twg);
+      uint4* dst = reinterpret_cast<uint4*>(tws);
+      for (int i = tid; i < NTW / 2; i += NT) dst[i] = __ldg(src + i);
+      __syncthreads();
+    }
+    const Mod32 md{inf.p, 2 * inf.p};
+    mbar_wait(mbar, phase);
+    phase ^= 1u;
+    uint32_t x[E];
+    const uint32_t* nxt = q + 1 < qend ? in + poly(q + 1) : nullptr;
+    auto hook = [&]() {
+      if (tid == 0 && nxt) bulk_g2s(stage, nxt, N * 4, mbar);
+    };
+    if constexpr (FWD) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) x[e] = to_lazy4(stage[tid + e * NT], inf);
+      cta_fwd<LOGN, 4, Mod32>(md, x, sm, tws, twg, hook, LOGN - G_::RLAST);
+#pragma unroll
+      for (int e = 0; e < E; ++e) x[e] = md.canon4(x[e]);
+      store_row_vec<LOGN, 4, uint32_t>(out + poly(q), tid, x);
+    } else {
+      load_row_vec<LOGN, 4, uint32_t>(stage, tid, x);
+      cta_inv<LOGN, 4, Mod32>(md, x, sm, tws, inf.ninv, inf.wn, twg, hook);
+      uint32_t* dst = out + poly(q);
+#pragma unroll
+      for (int e = 0; e < E; ++e) dst[tid + e * NT] = md.subp(x[e]);
+    }
+  }
+}
+
+static int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+  }
+  return n;
+}
+
+template <int LOGN>
+static int launch_b32(bool fwd, const uint32_t* in, uint32_t* out, int64_t batch, int nprimes,
+                      int prime_base, const uint2* tw, const Prime32Info* info, cudaStream_t st) {
+  typedef Geo<LOGN, 4> G_;
+  const size_t smem = (size_t)(1 << (LOGN - G_::RLAST)) * sizeof(uint2) +
+                      (size_t)((spad_size(G_::N) + 3) & ~3) * 4 + (size_t)G_::N * 4 + 16;
+  auto kern = fwd ? k_ntt32_b<LOGN, true> : k_ntt32_b<LOGN, false>;
+  HEFV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G_::NT, smem) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  const int64_t P = batch * nprimes;
+  const int64_t slots = (int64_t)sm_count() * per_sm;
+  const unsigned grid = (unsigned)(P < slots ? P : slots);
+  kern<<<grid, G_::NT, smem, st>>>(in, out, batch, nprimes, prime_base, tw, info);
+  HEFV_LAUNCH_CHECK("k_ntt32_b");
+  return 0;
+}
+
 template <int LOGN, int LOGE, class M>
 static int launch_one(bool fwd, const typename M::T* in, typename M::T* out, int64_t batch,
                       int nprimes, int prime_base, int natural, const typename M::Tw* tw,
@@ -91,6 +211,14 @@ static int launch_one(bool fwd, const typename M::T* in, typename M::T* out, int
   const size_t smem = (size_t)spad_size(G_::N) * sizeof(typename M::T);
   const int64_t total = batch * nprimes;
   if (total <= 0) return 0;
+  if constexpr (sizeof(typename M::T) == 4 && LOGN >= 10 && LOGN <= 14 && LOGE == 4) {
+    // twiddles of the 32-bit set: fwd and inverse tables have the same type
+    if (!natural)
+      return launch_b32<LOGN>(fwd, reinterpret_cast<const uint32_t*>(in),
+                              reinterpret_cast<uint32_t*>(out), batch, nprimes, prime_base,
+                              reinterpret_cast<const uint2*>(tw),
+                              reinterpret_cast<const Prime32Info*>(info), st);
+  }
   if (total > 0x7fffffff) return fail("ntt: batch too large");
   if (fwd) {
     auto kern = k_ntt_fwd<LOGN, LOGE, M>;
