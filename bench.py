@@ -287,7 +287,7 @@ def run_ours(args, rank, local_rank, world):
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = _cpu_baseline_single(params, counts)
-        ntt = None if args.no_ntt else _ntt_microbench()
+        ntt = None if args.no_ntt else _ntt_microbench(peak)
         result = {
             "metric": METRIC, "value": round(step_ms, 3), "unit": "ms",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -321,7 +321,7 @@ def _int_peak() -> dict:
     sys.path.insert(0, str(ROOT / "tools"))
     from probe_int import measure
 
-    names = ["imad", "imad_hi", "imad_wide", "iadd3", "shoup_butterfly"]
+    names = ["imad", "imad_hi", "imad_wide", "iadd3", "shoup_butterfly", "shoup_butterfly64"]
     out = {n: measure(k) / 1e12 for k, n in enumerate(names) if n != "iadd3"}
     torch.cuda.synchronize()
     return out
@@ -366,8 +366,11 @@ def _cpu_baseline_single(params, counts) -> dict:
             "wall_s": round(time.perf_counter() - t0, 1)}
 
 
-def _ntt_microbench():
-    """Config 4 secondary: batched forward/inverse NTT polys/s (device order)."""
+def _ntt_microbench(peaks=None):
+    """Config 4 secondary: batched forward/inverse NTT polys/s (device order),
+    with each entry's roofline fraction: per-limb work (N/2) log2 N + N
+    modmuls against the measured lazy Shoup butterfly rate of
+    the word size (32-bit or 64-bit)."""
     import ctypes as C
 
     import torch
@@ -376,7 +379,7 @@ def _ntt_microbench():
     from paper_1901_10074_b200.ring import find_ntt_primes, root_of_unity
 
     lib = nat.load()
-    res = {}
+    res, fracs = {}, {}
     for log_n, bits, L, batch in [(16, 60, 8, 64), (14, 60, 8, 256), (12, 50, 8, 1024),
                                   (14, 30, 22, 256)]:
         n = 1 << log_n
@@ -408,9 +411,19 @@ def _ntt_microbench():
             b.record()
             torch.cuda.synchronize()
             ms = a.elapsed_time(b) / 5
-            res[f"N=2^{log_n},{bits}-bit,L={L},batch={batch},{name}"] = round(batch * L / (ms * 1e-3), 1)
+            ps = batch * L / (ms * 1e-3)
+            key = f"N=2^{log_n},{bits}-bit,L={L},batch={batch},{name}"
+            res[key] = round(ps, 1)
+            if peaks:
+                pk = peaks["shoup_butterfly64" if wide else "shoup_butterfly"]
+                tm = ps * ((n // 2) * log_n + n) / 1e12
+                fracs[key] = {"Tmodmul_s": round(tm, 3), "peak": round(pk, 3),
+                              "frac": round(tm / pk, 3)}
         lib.hefv_ctx_destroy(h)
-    return {"unit": "limb-polys/s", **res}
+    out = {"unit": "limb-polys/s", **res}
+    if peaks:
+        out["roofline"] = fracs
+    return out
 
 
 # ---------------------------------------------------------------------------
