@@ -89,15 +89,30 @@ __device__ __forceinline__ void fwd_full_pass(const M& md, typename M::T* x, int
 #pragma unroll
   for (int l = 0; l < LOGE; ++l) {
     const int half = G_::E >> (l + 1);
-    // the 2^l twiddles of this stage are contiguous: 16-byte loads
-    typename M::Tw w[1 << (LOGE - 1)];
-    load_tw_run<typename M::Tw, (1 << (LOGE - 1))>(tw + (1 << (s0 + l)) + (G << l), w, 1 << l);
+    if constexpr (sizeof(typename M::Tw) > 8) {
+      // 64-bit primes: one 16-byte twiddle per butterfly group, loaded where
+      // used (an array of 16-byte pairs would be placed in local memory)
+      const typename M::Tw* twb = tw + (1 << (s0 + l)) + (G << l);
 #pragma unroll
-    for (int u = 0; u < (1 << l); ++u) {
+      for (int u = 0; u < (1 << l); ++u) {
+        const typename M::Tw wu = twb[u];
 #pragma unroll
-      for (int e0 = 0; e0 < half; ++e0) {
-        const int e = u * 2 * half + e0;
-        md.ct(x[e], x[e + half], w[u]);
+        for (int e0 = 0; e0 < half; ++e0) {
+          const int e = u * 2 * half + e0;
+          md.ct(x[e], x[e + half], wu);
+        }
+      }
+    } else {
+      // the 2^l twiddles of this stage are contiguous: 16-byte loads
+      typename M::Tw w[1 << (LOGE - 1)];
+      load_tw_run<typename M::Tw, (1 << (LOGE - 1))>(tw + (1 << (s0 + l)) + (G << l), w, 1 << l);
+#pragma unroll
+      for (int u = 0; u < (1 << l); ++u) {
+#pragma unroll
+        for (int e0 = 0; e0 < half; ++e0) {
+          const int e = u * 2 * half + e0;
+          md.ct(x[e], x[e + half], w[u]);
+        }
       }
     }
   }
@@ -117,21 +132,38 @@ __device__ __forceinline__ void fwd_last_pass(const M& md, typename M::T* x, int
 #pragma unroll
   for (int l = 0; l < R; ++l) {
     const int half = (1 << R) >> (l + 1);
-    typename M::Tw w[BLK << (R - 1)];
     // stages whose table slice lies below 2^split_log read `tw` (e.g. a shared
     // copy), the others `tw_hi` (global, through L1)
     const typename M::Tw* src = (tw_hi == nullptr || s0 + l + 1 <= split_log) ? tw : tw_hi;
-    load_tw_run<typename M::Tw, (BLK << (R - 1))>(src + (1 << (s0 + l)) + ((tid * BLK) << l), w,
-                                                  BLK << l);
+    if constexpr (sizeof(typename M::Tw) > 8) {
+      const typename M::Tw* twb = src + (1 << (s0 + l)) + ((tid * BLK) << l);
 #pragma unroll
-    for (int b = 0; b < BLK; ++b) {
-      typename M::T* xb = x + b * (1 << R);
+      for (int b = 0; b < BLK; ++b) {
+        typename M::T* xb = x + b * (1 << R);
 #pragma unroll
-      for (int u = 0; u < (1 << l); ++u) {
+        for (int u = 0; u < (1 << l); ++u) {
+          const typename M::Tw wu = twb[(b << l) + u];
 #pragma unroll
-        for (int e0 = 0; e0 < half; ++e0) {
-          const int e = u * 2 * half + e0;
-          md.ct(xb[e], xb[e + half], w[(b << l) + u]);
+          for (int e0 = 0; e0 < half; ++e0) {
+            const int e = u * 2 * half + e0;
+            md.ct(xb[e], xb[e + half], wu);
+          }
+        }
+      }
+    } else {
+      typename M::Tw w[BLK << (R - 1)];
+      load_tw_run<typename M::Tw, (BLK << (R - 1))>(src + (1 << (s0 + l)) + ((tid * BLK) << l),
+                                                    w, BLK << l);
+#pragma unroll
+      for (int b = 0; b < BLK; ++b) {
+        typename M::T* xb = x + b * (1 << R);
+#pragma unroll
+        for (int u = 0; u < (1 << l); ++u) {
+#pragma unroll
+          for (int e0 = 0; e0 < half; ++e0) {
+            const int e = u * 2 * half + e0;
+            md.ct(xb[e], xb[e + half], w[(b << l) + u]);
+          }
         }
       }
     }
@@ -283,18 +315,36 @@ __device__ __forceinline__ void inv_last_pass(const M& md, typename M::T* x, int
       }
       continue;
     }
-    typename M::Tw w[BLK << (R - 1)];
-    load_tw_run<typename M::Tw, (BLK << (R - 1))>(itw + (1 << (s0 + l)) + ((tid * BLK) << l), w,
-                                                  BLK << l);
+    if constexpr (sizeof(typename M::Tw) > 8) {
+      // 64-bit primes: twiddles loaded where used (see fwd_full_pass)
+      const typename M::Tw* twb = itw + (1 << (s0 + l)) + ((tid * BLK) << l);
 #pragma unroll
-    for (int b = 0; b < BLK; ++b) {
-      typename M::T* xb = x + b * (1 << R);
+      for (int b = 0; b < BLK; ++b) {
+        typename M::T* xb = x + b * (1 << R);
 #pragma unroll
-      for (int u = 0; u < (1 << l); ++u) {
+        for (int u = 0; u < (1 << l); ++u) {
+          const typename M::Tw wu = twb[(b << l) + u];
 #pragma unroll
-        for (int e0 = 0; e0 < half; ++e0) {
-          const int e = u * 2 * half + e0;
-          md.gs(xb[e], xb[e + half], w[(b << l) + u]);
+          for (int e0 = 0; e0 < half; ++e0) {
+            const int e = u * 2 * half + e0;
+            md.gs(xb[e], xb[e + half], wu);
+          }
+        }
+      }
+    } else {
+      typename M::Tw w[BLK << (R - 1)];
+      load_tw_run<typename M::Tw, (BLK << (R - 1))>(itw + (1 << (s0 + l)) + ((tid * BLK) << l), w,
+                                                    BLK << l);
+#pragma unroll
+      for (int b = 0; b < BLK; ++b) {
+        typename M::T* xb = x + b * (1 << R);
+#pragma unroll
+        for (int u = 0; u < (1 << l); ++u) {
+#pragma unroll
+          for (int e0 = 0; e0 < half; ++e0) {
+            const int e = u * 2 * half + e0;
+            md.gs(xb[e], xb[e + half], w[(b << l) + u]);
+          }
         }
       }
     }
