@@ -176,12 +176,13 @@ struct Redc {
 //
 // K: digits per point (compile time, even; ring rows k..K-1 are zeroed once
 // and their key words are zero, so padded pairs contribute nothing).
-// Warps 0..K-1 consume (warp w = target prime j when w < k), warp K computes
-// the x-pair sums, warp K+1 streams each ciphertext's k x 32-word digit tile
+// Warps 0..JW-1 consume (warp w = target prime j = blockIdx.z * JW + w when
+// j < k), warp JW computes the x-pair sums, warp JW+1 streams each
+// ciphertext's k x 32-word digit tile
 // with one bulk copy into a KSA_STAGES-deep ring (full / xready / empty
 // mbarriers, no CTA-wide barrier in the loop).
-template <int K>
-__global__ void __launch_bounds__(32 * (K + 2), 1)
+template <int K, int JW>
+__global__ void __launch_bounds__(32 * (JW + 2), 1)
     k_ksa_mac(const uint32_t* __restrict__ X, const uint32_t* __restrict__ kaux,
               uint32_t* __restrict__ Y, int64_t B, int k, int log_n, int aux_base,
               const Prime32Info* __restrict__ info) {
@@ -207,14 +208,14 @@ __global__ void __launch_bounds__(32 * (K + 2), 1)
     for (int s = 0; s < KSA_STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&xready[s], 1);
-      mbar_init(&empty[s], K + 1);
+      mbar_init(&empty[s], JW + 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int q = k * 32 + threadIdx.x; q < K * 32; q += blockDim.x)
     for (int s = 0; s < KSA_STAGES; ++s) ring[s][q] = 0u;
   __syncthreads();
-  if (w == K + 1) {  // producer
+  if (w == JW + 1) {  // producer
     if (lane == 0) {
       for (int r = 0; r < nb; ++r) {
         const int s = r % KSA_STAGES;
@@ -224,7 +225,7 @@ __global__ void __launch_bounds__(32 * (K + 2), 1)
     }
     return;
   }
-  if (w == K) {  // x-pair sums
+  if (w == JW) {  // x-pair sums
     for (int r = 0; r < nb; ++r) {
       const int s = r % KSA_STAGES;
       mbar_wait(&full[s], (uint32_t)((r / KSA_STAGES) & 1));
@@ -241,8 +242,9 @@ __global__ void __launch_bounds__(32 * (K + 2), 1)
     }
     return;
   }
-  const bool active = w < k;
-  const int j = active ? w : 0;
+  const int jw = (int)blockIdx.z * JW + w;  // this warp's target prime
+  const bool active = jw < k;
+  const int j = active ? jw : 0;
   Redc red;
   red.a = info[aux_base + t].p;
   {
@@ -524,13 +526,17 @@ static int run_ksa_e(hefv_ctx* c, const uint32_t* kaux, const uint32_t* dig, int
     }
     {
       dim3 grid((unsigned)(3 * (n >> 5)), (unsigned)((nb + KSA_MAC_CTS - 1) / KSA_MAC_CTS));
-      if (k == 22)
-        k_ksa_mac<22><<<grid, 32 * 24, 0, st>>>(X, kaux, Y, nb, k, c->log_n, ab, c->d_info32);
-      else if (k <= 16)
-        k_ksa_mac<16><<<grid, 32 * 18, 0, st>>>(X, kaux, Y, nb, k, c->log_n, ab, c->d_info32);
-      else
-        k_ksa_mac<KSA_KMAX><<<grid, 32 * (KSA_KMAX + 2), 0, st>>>(X, kaux, Y, nb, k, c->log_n,
-                                                                   ab, c->d_info32);
+      // consumer warps per CTA: all k target primes where the key registers
+      // fit (k <= 22), else the primes split over blockIdx.z
+      if (k == 22) {
+        k_ksa_mac<22, 22><<<grid, 32 * 24, 0, st>>>(X, kaux, Y, nb, k, c->log_n, ab, c->d_info32);
+      } else if (k <= 16) {
+        k_ksa_mac<16, 16><<<grid, 32 * 18, 0, st>>>(X, kaux, Y, nb, k, c->log_n, ab, c->d_info32);
+      } else {
+        dim3 g2(grid.x, grid.y, (unsigned)((k + 11) / 12));
+        k_ksa_mac<KSA_KMAX, 12><<<g2, 32 * 14, 0, st>>>(X, kaux, Y, nb, k, c->log_n, ab,
+                                                         c->d_info32);
+      }
       HEFV_LAUNCH_CHECK("k_ksa_mac");
     }
     {
