@@ -213,14 +213,19 @@ int hefv_add_part0(hefv_ctx* ctx, uint32_t* rows, int64_t row_stride, const int3
  * hefv_ks_aux_key: switch key (k, k, N) Montgomery device order (as for
  *   hefv_keyswitch) -> kaux (3, 2k, k, N) = NTT_{a_t}(iNTT_j(K_ji)), parts
  *   [body j | mask j].
- * hefv_keyswitch_aux: arguments as hefv_keyswitch, plus scratch of
- *   scratch_cts * 9 k N words (ciphertexts are processed in chunks of
- *   scratch_cts). */
+ * hefv_keyswitch_aux: arguments as hefv_keyswitch, plus
+ *   dig_slot: item b's digit rows come from digits + dig_slot[b] * dig_stride
+ *     (NULL: b * dig_stride);
+ *   galois_elt: if nonzero, the digits are sigma_g(c) of those rows -- the
+ *     automorphism of a rotation hop (fv.py:157-173) fused into the load;
+ *   scratch of scratch_cts * 9 k N words (ciphertexts are processed in chunks
+ *     of scratch_cts). */
 int hefv_ks_aux_setup(hefv_ctx* ctx, int32_t aux_base);
 int hefv_ks_aux_key(hefv_ctx* ctx, const uint32_t* kbody, const uint32_t* kmask, uint32_t* kaux,
                     void* stream);
 int hefv_keyswitch_aux(hefv_ctx* ctx, const uint32_t* kaux, const uint32_t* digits,
-                       int64_t dig_stride, uint32_t* out0, uint32_t* out1, int64_t out_stride,
+                       int64_t dig_stride, const int32_t* dig_slot, uint32_t galois_elt,
+                       uint32_t* out0, uint32_t* out1, int64_t out_stride,
                        const int32_t* slot, const uint32_t* adA0, const uint32_t* adA1,
                        int64_t adA_stride, const uint32_t* adB0, const uint32_t* adB1,
                        int64_t adB_stride, uint32_t* scratch, int64_t scratch_cts, int64_t B,

@@ -46,8 +46,8 @@ _SIGS = {
     "hefv_keyswitch": [_P, _P, _P, _P, _I64, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _I64, _I64, _P],
     "hefv_ks_aux_setup": [_P, _I32],
     "hefv_ks_aux_key": [_P, _P, _P, _P, _P],
-    "hefv_keyswitch_aux": [_P, _P, _P, _I64, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _I64, _P,
-                           _I64, _I64, _P],
+    "hefv_keyswitch_aux": [_P, _P, _P, _I64, _P, _U32, _P, _P, _I64, _P, _P, _P, _I64, _P, _P,
+                           _I64, _P, _I64, _I64, _P],
     "hefv_keygen_digit": [_P, _P, _P, _I32, _P, _P, _P, _P, _P, _P],
     "hefv_mult_tensor": [_P, _P, _P, _P, _P, _P],
     "hefv_mult_tensor_many": [_P, _P, _I64, _P, _I64, _P, _P, _I64, _P],

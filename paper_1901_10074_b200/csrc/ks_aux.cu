@@ -83,7 +83,8 @@ __device__ __forceinline__ void cp_async_wait() {
 // right after the current transform's first CTA barrier.
 template <int LOGN, int LOGE>
 __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
-    k_ksa_fwd(const uint32_t* __restrict__ digits, int64_t dig_stride, uint32_t* __restrict__ X,
+    k_ksa_fwd(const uint32_t* __restrict__ digits, int64_t dig_stride,
+              const int32_t* __restrict__ dslot, uint32_t ginv, uint32_t* __restrict__ X,
               int64_t B, int k, int aux_base, const uint2* __restrict__ tw_all,
               const Prime32Info* __restrict__ info) {
   typedef Geo<LOGN, LOGE> G_;
@@ -114,16 +115,32 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
     for (int q = tid; q < NTW / 2; q += NT) dst[q] = __ldg(src + q);
   }
   __syncthreads();
-  if (tid == 0) bulk_g2s(stage, digits + bbeg * dig_stride + (size_t)i * N, N * 4, mbar);
+  // digit row i of ciphertext b (through the slot map when given)
+  auto row = [&](int64_t b) {
+    return digits + (dslot ? (int64_t)dslot[b] : b) * dig_stride + (size_t)i * N;
+  };
+  const uint32_t pdig = info[i].p;  // the digit's own prime (negation under sigma)
+  if (tid == 0) bulk_g2s(stage, row(bbeg), N * 4, mbar);
   uint32_t phase = 0;
   for (int64_t b = bbeg; b < bend; ++b) {
     mbar_wait(mbar, phase);
     phase ^= 1u;
     uint32_t x[E];
     // c_i < p_i < 2^30 <= 4 a_t: a valid lazy input
+    if (ginv) {
+      // fused Galois automorphism x -> x^g (fv.py:157-173): coefficient m of
+      // sigma(c) is c[m g^-1 mod 2N], negated mod p_i when that index >= N
 #pragma unroll
-    for (int e = 0; e < E; ++e) x[e] = stage[tid + e * NT];
-    const uint32_t* nxt = b + 1 < bend ? digits + (b + 1) * dig_stride + (size_t)i * N : nullptr;
+      for (int e = 0; e < E; ++e) {
+        const uint32_t j1 = ((uint32_t)(tid + e * NT) * ginv) & (2u * N - 1u);
+        const uint32_t v = stage[j1 & (N - 1)];
+        x[e] = (j1 & N) ? (v ? pdig - v : 0u) : v;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) x[e] = stage[tid + e * NT];
+    }
+    const uint32_t* nxt = b + 1 < bend ? row(b + 1) : nullptr;
     auto hook = [&]() {
       if (tid == 0 && nxt) bulk_g2s(stage, nxt, N * 4, mbar);
     };
@@ -463,6 +480,7 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
 
 template <int LOGN, int LF, int LI>
 static int run_ksa_e(hefv_ctx* c, const uint32_t* kaux, const uint32_t* dig, int64_t ds,
+                     const int32_t* dslot, uint32_t ginv,
                      uint32_t* o0, uint32_t* o1, int64_t os, const int32_t* slot,
                      const uint32_t* a0, const uint32_t* a1, int64_t as, const uint32_t* b0,
                      const uint32_t* b1, int64_t bs, uint32_t* scratch, int64_t scratch_cts,
@@ -470,6 +488,7 @@ static int run_ksa_e(hefv_ctx* c, const uint32_t* kaux, const uint32_t* dig, int
 
 template <int LOGN>
 static int run_ksa(hefv_ctx* c, const uint32_t* kaux, const uint32_t* dig, int64_t ds,
+                   const int32_t* dslot, uint32_t ginv,
                    uint32_t* o0, uint32_t* o1, int64_t os, const int32_t* slot,
                    const uint32_t* a0, const uint32_t* a1, int64_t as, const uint32_t* b0,
                    const uint32_t* b1, int64_t bs, uint32_t* scratch, int64_t scratch_cts,
@@ -482,21 +501,22 @@ static int run_ksa(hefv_ctx* c, const uint32_t* kaux, const uint32_t* dig, int64
       return v ? atoi(v) : 0;
     }();
     if (e32 == 1)
-      return run_ksa_e<LOGN, 5, 4>(c, kaux, dig, ds, o0, o1, os, slot, a0, a1, as, b0, b1, bs,
+      return run_ksa_e<LOGN, 5, 4>(c, kaux, dig, ds, dslot, ginv, o0, o1, os, slot, a0, a1, as, b0, b1, bs,
                                    scratch, scratch_cts, B, st);
     if (e32 == 2)
-      return run_ksa_e<LOGN, 4, 5>(c, kaux, dig, ds, o0, o1, os, slot, a0, a1, as, b0, b1, bs,
+      return run_ksa_e<LOGN, 4, 5>(c, kaux, dig, ds, dslot, ginv, o0, o1, os, slot, a0, a1, as, b0, b1, bs,
                                    scratch, scratch_cts, B, st);
     if (e32 == 3)
-      return run_ksa_e<LOGN, 5, 5>(c, kaux, dig, ds, o0, o1, os, slot, a0, a1, as, b0, b1, bs,
+      return run_ksa_e<LOGN, 5, 5>(c, kaux, dig, ds, dslot, ginv, o0, o1, os, slot, a0, a1, as, b0, b1, bs,
                                    scratch, scratch_cts, B, st);
   }
-  return run_ksa_e<LOGN, 4, 4>(c, kaux, dig, ds, o0, o1, os, slot, a0, a1, as, b0, b1, bs,
+  return run_ksa_e<LOGN, 4, 4>(c, kaux, dig, ds, dslot, ginv, o0, o1, os, slot, a0, a1, as, b0, b1, bs,
                                scratch, scratch_cts, B, st);
 }
 
 template <int LOGN, int LF, int LI>
 static int run_ksa_e(hefv_ctx* c, const uint32_t* kaux, const uint32_t* dig, int64_t ds,
+                     const int32_t* dslot, uint32_t ginv,
                      uint32_t* o0, uint32_t* o1, int64_t os, const int32_t* slot,
                      const uint32_t* a0, const uint32_t* a1, int64_t as, const uint32_t* b0,
                      const uint32_t* b1, int64_t bs, uint32_t* scratch, int64_t scratch_cts,
@@ -521,7 +541,8 @@ static int run_ksa_e(hefv_ctx* c, const uint32_t* kaux, const uint32_t* dig, int
     const int64_t nb = (B - c0) < chunk ? (B - c0) : chunk;
     {
       dim3 grid((unsigned)(3 * k), (unsigned)((nb + KSA_FWD_CTS - 1) / KSA_FWD_CTS));
-      kf<<<grid, GF::NT, smf, st>>>(dig + c0 * ds, ds, X, nb, k, ab, c->d_tw32, c->d_info32);
+      kf<<<grid, GF::NT, smf, st>>>(dslot ? dig : dig + c0 * ds, ds, dslot ? dslot + c0 : nullptr,
+                                    ginv, X, nb, k, ab, c->d_tw32, c->d_info32);
       HEFV_LAUNCH_CHECK("k_ksa_fwd");
     }
     {
@@ -675,7 +696,8 @@ int hefv_ks_aux_key(hefv_ctx* c, const uint32_t* kbody, const uint32_t* kmask, u
 }
 
 int hefv_keyswitch_aux(hefv_ctx* c, const uint32_t* kaux, const uint32_t* digits,
-                       int64_t dig_stride, uint32_t* out0, uint32_t* out1, int64_t out_stride,
+                       int64_t dig_stride, const int32_t* dig_slot, uint32_t galois_elt,
+                       uint32_t* out0, uint32_t* out1, int64_t out_stride,
                        const int32_t* slot, const uint32_t* adA0, const uint32_t* adA1,
                        int64_t adA_stride, const uint32_t* adB0, const uint32_t* adB1,
                        int64_t adB_stride, uint32_t* scratch, int64_t scratch_cts, int64_t B,
@@ -684,7 +706,16 @@ int hefv_keyswitch_aux(hefv_ctx* c, const uint32_t* kaux, const uint32_t* digits
   if (B <= 0) return 0;
   if (scratch_cts < 1) return fail("hefv_keyswitch_aux: scratch must hold at least one ciphertext");
   cudaStream_t st = as_stream(stream);
-  HEFV_KSA_DISPATCH(run_ksa, c, kaux, digits, dig_stride, out0, out1, out_stride, slot, adA0,
+  uint32_t ginv = 0;  // inverse of the Galois element mod 2N (0: no automorphism)
+  if (galois_elt) {
+    if ((galois_elt & 1u) == 0) return fail("hefv_keyswitch_aux: galois element must be odd");
+    const uint32_t two_n = 2u * (uint32_t)c->n;
+    const uint32_t g = galois_elt % two_n;
+    uint32_t inv = 1;
+    for (int it = 0; it < 6; ++it) inv *= 2u - g * inv;
+    ginv = inv & (two_n - 1u);
+  }
+  HEFV_KSA_DISPATCH(run_ksa, c, kaux, digits, dig_stride, dig_slot, ginv, out0, out1, out_stride, slot, adA0,
                     adA1, adA_stride, adB0, adB1, adB_stride, scratch, scratch_cts, B, st)
 }
 

@@ -695,17 +695,14 @@ class FvBackend(SlotBackend):
         return [1 << j for j in range(offset.bit_length()) if offset >> j & 1]
 
     def _hop(self, dev, off):
-        ctx = self.ctx
-        g = galois_element(off, ctx.n)
-        scratch = ctx.empty(2, ctx.k, ctx.n)
-        ctx.call("hefv_automorph", dev.data_ptr(), 0, None, scratch.data_ptr(), 2, g, 1,
-                 ctx.stream())
-        from .planner import keyswitch_call
+        from .planner import rotation_keyswitch
 
+        ctx = self.ctx
+        scratch = ctx.empty(2, ctx.k, ctx.n)
         out = ctx.empty(2, ctx.k, ctx.n)
-        key = self.keys.galois[off]
-        keyswitch_call(ctx, key, scratch[1].data_ptr(), 0, out[0].data_ptr(), out[1].data_ptr(), 0,
-                       None, scratch[0].data_ptr(), None, 0, None, None, 0, 1)
+        rotation_keyswitch(ctx, self.keys.galois[off], dev.data_ptr(), 0, None,
+                           galois_element(off, ctx.n), 1, out[0].data_ptr(), out[1].data_ptr(), 0,
+                           None, None, None, 0, scratch.data_ptr())
         return out
 
     def _rotate(self, a, offset, level):

@@ -48,11 +48,14 @@ STATS = {"ks_launches": 0, "ks_cts": 0}
 KS_EVENTS = None
 
 
-def keyswitch_call(ctx, key, *args):
+def keyswitch_call(ctx, key, *args, dig_slot=None, galois=0):
     """One batched key switch under ``key`` (a SwitchKey) with the planner's
     accounting; ``args`` are hefv_keyswitch's after the key pointers (the
     batch size last).  Keys with an aux-basis form go through
-    hefv_keyswitch_aux (same limbs, fewer transforms)."""
+    hefv_keyswitch_aux (same limbs, fewer transforms), which can also read
+    the digit rows through a slot map and apply a Galois automorphism on the
+    fly (``dig_slot`` device pointer, ``galois`` element); the per-prime
+    kernel needs its digits materialised."""
     import torch
 
     batch = int(args[-1])
@@ -61,8 +64,11 @@ def keyswitch_call(ctx, key, *args):
     if key.aux_dev is not None:
         scratch, cap = _ks_workspace(ctx, batch)
         name = "hefv_keyswitch_aux"
-        full = (key.aux_dev.data_ptr(), *args[:-1], scratch.data_ptr(), cap, batch)
+        full = (key.aux_dev.data_ptr(), args[0], args[1], dig_slot, int(galois), *args[2:-1],
+                scratch.data_ptr(), cap, batch)
     else:
+        if dig_slot is not None or galois:
+            raise ValueError("the per-prime key switch needs materialised digits")
         name = "hefv_keyswitch"
         full = (key.body_dev.data_ptr(), key.mask_dev.data_ptr(), *args)
     if KS_EVENTS is not None:
@@ -74,6 +80,27 @@ def keyswitch_call(ctx, key, *args):
         KS_EVENTS.append((e0, e1, batch))
     else:
         ctx.call(name, *full, ctx.stream())
+
+
+def rotation_keyswitch(ctx, key, src, src_stride, slot, g, B, out0, out1, out_stride, out_slot,
+                       adB0, adB1, adB_stride, scratch):
+    """One Galois hop of B ciphertexts (fv.py:417-432, 157-173):
+    out[out_slot b] = KS(sigma_g(c1)) + (sigma_g(c0), 0) + adB[out_slot b]
+    with c = the ciphertext at src + slot[b] * src_stride (words; slot may be
+    None).  With an aux-basis key only sigma_g(c0) is materialised (into
+    ``scratch``, >= B k N words) and sigma_g(c1) is applied inside the key
+    switch's digit load; otherwise both parts go through ``scratch`` (>= 2 B
+    k N words)."""
+    stack = ctx.k * ctx.n
+    st = ctx.stream()
+    if key.aux_dev is not None:
+        ctx.call("hefv_automorph", src, src_stride, slot, scratch, 1, g, B, st)
+        keyswitch_call(ctx, key, src + stack * 4, src_stride, out0, out1, out_stride, out_slot,
+                       scratch, None, stack, adB0, adB1, adB_stride, B, dig_slot=slot, galois=g)
+    else:
+        ctx.call("hefv_automorph", src, src_stride, slot, scratch, 2, g, B, st)
+        keyswitch_call(ctx, key, scratch + stack * 4, 2 * stack, out0, out1, out_stride, out_slot,
+                       scratch, None, 2 * stack, adB0, adB1, adB_stride, B)
 
 
 KS_WORKSPACE_BYTES = 16 << 30  # ~1300 ciphertexts per chunk at retina (fewer kernel tails)
@@ -376,14 +403,12 @@ def _run_rows(backend, rows, x, seg_lists, active, m_arr, off_arr, bias_arr, out
         a0 = acc.data_ptr()
         a1 = a0 + stack * 4
         s0 = scr.data_ptr()
-        s1 = s0 + stack * 4
         for j in range(n_iter):
             shift = 1 << j
             key = keys[shift]
             g = galois_element(shift, n)
-            ctx.call("hefv_automorph", a0, ct_words, None, s0, 2, g, B, st)
-            keyswitch_call(ctx, key, s1, ct_words,
-                           a0, a1, ct_words, None, s0, None, ct_words, a0, a1, ct_words, B)
+            rotation_keyswitch(ctx, key, a0, ct_words, None, g, B, a0, a1, ct_words, None, a0, a1,
+                               ct_words, s0)
         # ---- 4. biases and the e0 mask ---------------------------------------------
         bias_rows = [bi for bi, i in enumerate(tile) if bias_arr[i]]
         if bias_rows:
@@ -417,10 +442,8 @@ def _run_rows(backend, rows, x, seg_lists, active, m_arr, off_arr, bias_arr, out
             sub = scr[:nb]
             b0 = sub.data_ptr()
             key = keys[h]
-            ctx.call("hefv_automorph", a0, ct_words, d_slot.data_ptr(), b0, 2,
-                     galois_element(h, n), nb, st)
-            keyswitch_call(ctx, key, b0 + stack * 4, ct_words, a0, a1, ct_words, d_slot.data_ptr(),
-                           b0, None, ct_words, None, None, 0, nb)
+            rotation_keyswitch(ctx, key, a0, ct_words, d_slot.data_ptr(), galois_element(h, n), nb,
+                               a0, a1, ct_words, d_slot.data_ptr(), None, None, 0, b0)
         del scr
         # ---- 6. sum pieces into their output ciphertexts -----------------------------
         ms = m_arr[tile]

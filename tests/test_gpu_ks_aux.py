@@ -59,8 +59,8 @@ def _both(params, B, seed, extremes=False):
             per_ct = 9 * k * n
             cap = max(1, B // 3)  # force several chunks
             ws = torch.empty(cap * per_ct, dtype=torch.int32, device="cuda")
-            ctx.call("hefv_keyswitch_aux", key.aux_dev.data_ptr(), *args, ws.data_ptr(), cap, B,
-                     ctx.stream())
+            ctx.call("hefv_keyswitch_aux", key.aux_dev.data_ptr(), args[0], args[1], None, 0,
+                     *args[2:], ws.data_ptr(), cap, B, ctx.stream())
         else:
             ctx.call("hefv_keyswitch", key.body_dev.data_ptr(), key.mask_dev.data_ptr(), *args, B,
                      ctx.stream())
@@ -98,3 +98,50 @@ def test_aux_keyswitch_retina_profile_rotations_match_golden_path():
         finally:
             os.environ.pop("HEFV_KS_AUX", None)
     assert digs[0] == digs[1]
+
+
+@pytest.mark.parametrize("logn,k", [(14, 22), (12, 17)])
+def test_aux_keyswitch_fused_automorphism_with_slot_map(logn, k):
+    """Digits read through a slot map with the Galois automorphism applied in
+    the load (hefv_keyswitch_aux dig_slot/galois) equal the per-prime kernel
+    on materialised sigma_g(c1) rows (hefv_automorph)."""
+    import torch
+
+    from paper_1901_10074_b200.fv import FvBackend
+    from paper_1901_10074_b200.ring import galois_element
+
+    be = FvBackend(_params(logn, k), rng=np.random.default_rng(7))
+    ctx = be.ctx
+    n = ctx.n
+    stack = k * n
+    rng = np.random.default_rng(8)
+    R, B = 9, 6
+    p = np.array(ctx.q_primes, dtype=np.int64)[None, None, :, None]
+    src = rng.integers(0, 1 << 62, (R, 2, k, n)) % p
+    src[0, 1, :, ::3] = 0  # zero coefficients (sigma must keep them 0, not p)
+    slot = rng.permutation(R)[:B].astype(np.int32)
+    d_src = torch.from_numpy(src.astype(np.int32)).cuda()
+    d_slot = torch.from_numpy(slot).cuda()
+    off = 4 if logn == 14 else 2
+    key = be.keys.galois[off]
+    g = galois_element(off, n)
+    outs = []
+    for fused in (True, False):
+        out = torch.zeros((R, 2, k, n), dtype=torch.int32, device="cuda")
+        if fused:
+            per_ct = 9 * stack
+            ws = torch.empty(2 * per_ct, dtype=torch.int32, device="cuda")  # 2-ct chunks
+            ctx.call("hefv_keyswitch_aux", key.aux_dev.data_ptr(), d_src[0, 1].data_ptr(),
+                     2 * stack, d_slot.data_ptr(), g, out[0, 0].data_ptr(), out[0, 1].data_ptr(),
+                     2 * stack, d_slot.data_ptr(), None, None, 0, None, None, 0, ws.data_ptr(),
+                     2, B, ctx.stream())
+        else:
+            sig = torch.empty((B, 2, k, n), dtype=torch.int32, device="cuda")
+            ctx.call("hefv_automorph", d_src.data_ptr(), 2 * stack, d_slot.data_ptr(),
+                     sig.data_ptr(), 2, g, B, ctx.stream())
+            ctx.call("hefv_keyswitch", key.body_dev.data_ptr(), key.mask_dev.data_ptr(),
+                     sig[0, 1].data_ptr(), 2 * stack, out[0, 0].data_ptr(), out[0, 1].data_ptr(),
+                     2 * stack, d_slot.data_ptr(), None, None, 0, None, None, 0, B, ctx.stream())
+        torch.cuda.synchronize()
+        outs.append(out.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])

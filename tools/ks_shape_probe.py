@@ -45,7 +45,8 @@ if key.aux_dev is not None:
 def ks():
     args = (s1, 2 * stack, a0, a1, 2 * stack, None, s0, None, 2 * stack, a0, a1, 2 * stack)
     if ws is not None:
-        ctx.call("hefv_keyswitch_aux", key.aux_dev.data_ptr(), *args, ws.data_ptr(), cap, B, st)
+        ctx.call("hefv_keyswitch_aux", key.aux_dev.data_ptr(), args[0], args[1], None, 0,
+                 *args[2:], ws.data_ptr(), cap, B, st)
     else:
         ctx.call("hefv_keyswitch", key.body_dev.data_ptr(), key.mask_dev.data_ptr(), *args, B, st)
 
