@@ -186,6 +186,7 @@ int hefv_ctx_create(hefv_ctx** out, uint32_t log_n, int32_t n32, const uint32_t*
       const u128 r = ((u128)1 << 64) % p;  // 2^64 mod p
       inf.r2 = (uint64_t)(r * r % p);
     }
+    inf.mu = (uint64_t)(((u128)1 << 64) / p);
     c->info64.push_back(inf);
   }
   // ---- upload

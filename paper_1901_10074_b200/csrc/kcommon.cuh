@@ -10,7 +10,7 @@ __device__ __forceinline__ uint32_t reduce_any(uint32_t x, const Prime32Info& i)
   return barrett62(x, i.p, i.mu);
 }
 __device__ __forceinline__ uint64_t reduce_any(uint64_t x, const Prime64Info& i) {
-  return x >= i.p ? x % i.p : x;
+  return x >= i.p ? barrett64(x, i.p, i.mu) : x;
 }
 
 template <class M>

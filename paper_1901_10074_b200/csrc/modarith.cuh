@@ -155,7 +155,16 @@ struct Prime64Info {
   ulonglong2 wn;
   uint64_t pinv_neg;  // -p^{-1} mod 2^64 (Montgomery)
   uint64_t r2;        // 2^128 mod p
+  uint64_t mu;        // floor(2^64 / p) (Barrett)
 };
+
+// x mod p for any x < 2^64 and 2 <= p < 2^62 without a division call:
+// q = hi(x mu) lies within 2 of floor(x / p), so x - q p < 3p.
+__device__ __forceinline__ uint64_t barrett64(uint64_t x, uint64_t p, uint64_t mu) {
+  uint64_t r = x - __umul64hi(x, mu) * p;
+  r = r >= p ? r - p : r;
+  return r >= p ? r - p : r;
+}
 
 // 64-bit Montgomery REDC of a*b (a < 2^64, b < p < 2^62): a*b*2^-64 mod p in [0, 2p).
 __device__ __forceinline__ uint64_t mont_mul64_lazy(uint64_t a, uint64_t b, uint64_t p,

@@ -298,7 +298,7 @@ __device__ __forceinline__ void cta_fwd(const M& md, typename M::T* x, typename 
 template <int LOGN, int LOGE, class M>
 __device__ __forceinline__ void inv_last_pass(const M& md, typename M::T* x, int tid,
                                               const typename M::Tw* __restrict__ itw,
-                                              typename M::Tw ninv, typename M::Tw wn) {
+                                              const typename M::Tw& ninv, const typename M::Tw& wn) {
   typedef Geo<LOGN, LOGE> G_;
   constexpr int R = G_::RLAST;
   constexpr int s0 = LOGN - R;
@@ -354,7 +354,7 @@ __device__ __forceinline__ void inv_last_pass(const M& md, typename M::T* x, int
 template <int LOGN, int LOGE, class M>
 __device__ __forceinline__ void inv_full_pass(const M& md, typename M::T* x, int pass, int tid,
                                               const typename M::Tw* __restrict__ itw,
-                                              typename M::Tw ninv, typename M::Tw wn) {
+                                              const typename M::Tw& ninv, const typename M::Tw& wn) {
   typedef Geo<LOGN, LOGE> G_;
   const int s0 = pass * LOGE;
   const int tsh = LOGN - s0 - LOGE;
@@ -393,7 +393,7 @@ __device__ __forceinline__ void inv_full_pass(const M& md, typename M::T* x, int
 template <int LOGN, int LOGE, class M, class Hook = NoHook>
 __device__ __forceinline__ void cta_inv(const M& md, typename M::T* x, typename M::T* sm,
                                         const typename M::Tw* __restrict__ itw,
-                                        typename M::Tw ninv, typename M::Tw wn,
+                                        const typename M::Tw& ninv, const typename M::Tw& wn,
                                         const typename M::Tw* __restrict__ itw_last = nullptr,
                                         const Hook& hook = Hook()) {
   typedef Geo<LOGN, LOGE> G_;

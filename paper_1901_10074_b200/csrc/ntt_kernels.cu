@@ -6,6 +6,8 @@
 // For 64-bit primes with N > 2^14 the polynomial (>= 256 KB) does not fit a
 // CTA's shared memory; those sizes run the two-kernel global-memory variant
 // at the end of this file (column pass + row pass, each CTA-resident).
+#include <cstdlib>
+
 #include "../../include/hefv.h"
 #include "internal.h"
 #include "ntt.cuh"
@@ -172,6 +174,97 @@ __global__ void __launch_bounds__(Geo<LOGN, 4>::NT, 1024 / Geo<LOGN, 4>::NT)
   }
 }
 
+// ---- batched device-order path for 64-bit primes, 2^10 <= N <= 2^14 --------
+// Same persistent prime-major schedule as k_ntt32_b.  STAGE: the prime's
+// full-pass twiddles (16-byte Shoup pairs) are staged in shared memory next
+// to the tile (64 KB at N = 2^14; loading them from L2 inside the passes
+// left the 2^14 transform long-scoreboard bound).  The next polynomial is
+// prefetched into L2 by one bulk prefetch per transform; a shared staging
+// copy as in k_ntt32_b does not fit next to a 64-bit tile.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+template <int LOGN>
+struct Ntt64B {
+  typedef Geo<LOGN, 4> G_;
+  static constexpr int NTW = 1 << (LOGN - G_::RLAST);
+  static constexpr size_t tw_bytes(bool stage) { return stage ? (size_t)NTW * 16 : 0; }
+  static constexpr size_t smem(bool stage) {
+    return tw_bytes(stage) + (size_t)((spad_size(G_::N) + 1) & ~1) * 8;
+  }
+};
+
+template <int LOGN, bool FWD, bool STAGE>
+__global__ void __launch_bounds__(Geo<LOGN, 4>::NT, LOGN >= 13 ? 1024 / Geo<LOGN, 4>::NT : 2)
+    k_ntt64_b(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, int64_t batch,
+              int nprimes, int prime_base, const ulonglong2* __restrict__ tw_all,
+              const Prime64Info* __restrict__ info) {
+  typedef Geo<LOGN, 4> G_;
+  constexpr int E = G_::E;
+  constexpr int NT = G_::NT;
+  constexpr int N = G_::N;
+  constexpr int NTW = Ntt64B<LOGN>::NTW;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  ulonglong2* tws = reinterpret_cast<ulonglong2*>(smraw);
+  uint64_t* sm = reinterpret_cast<uint64_t*>(smraw + Ntt64B<LOGN>::tw_bytes(STAGE));
+  const int tid = threadIdx.x;
+  const int64_t P = batch * nprimes;
+  const int64_t qbeg = P * blockIdx.x / gridDim.x;
+  const int64_t qend = P * (blockIdx.x + 1) / gridDim.x;
+  if (qbeg >= qend) return;
+  // prime-major work order q -> (prime j, batch index b), walked without
+  // divisions (a 64-bit division is a call that forces spills here)
+  int j = (int)(qbeg / batch);
+  int64_t b = qbeg - (int64_t)j * batch;
+  const int64_t pstride = (int64_t)nprimes * N;
+  const Prime64Info* ip = nullptr;
+  const ulonglong2* twg = nullptr;
+  uint64_t p = 0;
+  for (int64_t q = qbeg; q < qend; ++q) {
+    if (ip == nullptr || b == batch) {
+      if (ip != nullptr) {
+        b = 0;
+        ++j;
+      }
+      ip = info + prime_base + j;
+      p = ip->p;
+      twg = tw_all + (size_t)(prime_base + j) * N;
+      if constexpr (STAGE) {
+        __syncthreads();  // the previous prime's table is no longer read
+        for (int i = tid; i < NTW; i += NT) tws[i] = __ldg(twg + i);
+        __syncthreads();
+      }
+    }
+    const uint64_t* src = in + b * pstride + (int64_t)j * N;
+    uint64_t* dst = out + b * pstride + (int64_t)j * N;
+    if (tid == 0 && q + 1 < qend) {
+      const bool wrap = b + 1 == batch;
+      bulk_prefetch_l2(wrap ? in + (j + 1) * (int64_t)N : src + pstride, N * 8);
+    }
+    ++b;
+    const Mod64 md{p, 2 * p};
+    const ulonglong2* twf = STAGE ? tws : twg;
+    uint64_t x[E];
+    if constexpr (FWD) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const uint64_t v = src[tid + e * NT];
+        x[e] = v >= p ? barrett64(v, p, ip->mu) : v;
+      }
+      cta_fwd<LOGN, 4, Mod64>(md, x, sm, twf, twg, NoHook(), LOGN - G_::RLAST);
+#pragma unroll
+      for (int e = 0; e < E; ++e) x[e] = md.canon4(x[e]);
+      store_row_vec<LOGN, 4, uint64_t>(dst, tid, x);
+    } else {
+      load_row_vec<LOGN, 4, uint64_t>(src, tid, x);
+      cta_inv<LOGN, 4, Mod64>(md, x, sm, twf, ip->ninv, ip->wn, twg);
+#pragma unroll
+      for (int e = 0; e < E; ++e) dst[tid + e * NT] = md.subp(x[e]);
+    }
+  }
+}
+
 static int sm_count() {
   static int n = 0;
   if (n == 0) {
@@ -203,6 +296,43 @@ static int launch_b32(bool fwd, const uint32_t* in, uint32_t* out, int64_t batch
   return 0;
 }
 
+// 64-bit device-order transform variant: 0 = one CTA per polynomial
+// (k_ntt_fwd/inv), 1 = persistent with twiddles from L1/L2, 2 = persistent
+// with staged twiddles.  Default = the measured best per (N, direction) on a
+// B200 (60-bit primes, L = 8, batch 256-1024): persistent for 2^13 and the
+// 2^14 inverse (0.62-0.67 of the butterfly peak vs 0.57-0.61), one CTA per
+// polynomial elsewhere (staging never won).  HEFV_NTT64_B overrides.
+static int ntt64_mode(int log_n, bool fwd) {
+  static int env = -2;
+  if (env == -2) {
+    const char* v = std::getenv("HEFV_NTT64_B");
+    env = v ? std::atoi(v) : -1;
+  }
+  if (env >= 0) return env;
+  return (log_n == 13 || (log_n == 14 && !fwd)) ? 1 : 0;
+}
+
+template <int LOGN>
+static int launch_b64(bool fwd, const uint64_t* in, uint64_t* out, int64_t batch, int nprimes,
+                      int prime_base, const ulonglong2* tw, const Prime64Info* info, cudaStream_t st,
+                      bool stage) {
+  typedef Geo<LOGN, 4> G_;
+  const size_t smem = Ntt64B<LOGN>::smem(stage);
+  auto kern = fwd ? (stage ? k_ntt64_b<LOGN, true, true> : k_ntt64_b<LOGN, true, false>)
+                  : (stage ? k_ntt64_b<LOGN, false, true> : k_ntt64_b<LOGN, false, false>);
+  HEFV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G_::NT, smem) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  const int64_t P = batch * nprimes;
+  const int64_t slots = (int64_t)sm_count() * per_sm;
+  const unsigned grid = (unsigned)(P < slots ? P : slots);
+  kern<<<grid, G_::NT, smem, st>>>(in, out, batch, nprimes, prime_base, tw, info);
+  HEFV_LAUNCH_CHECK("k_ntt64_b");
+  return 0;
+}
+
 template <int LOGN, int LOGE, class M>
 static int launch_one(bool fwd, const typename M::T* in, typename M::T* out, int64_t batch,
                       int nprimes, int prime_base, int natural, const typename M::Tw* tw,
@@ -218,6 +348,14 @@ static int launch_one(bool fwd, const typename M::T* in, typename M::T* out, int
                               reinterpret_cast<uint32_t*>(out), batch, nprimes, prime_base,
                               reinterpret_cast<const uint2*>(tw),
                               reinterpret_cast<const Prime32Info*>(info), st);
+  }
+  if constexpr (sizeof(typename M::T) == 8 && LOGN >= 10 && LOGN <= 14 && LOGE == 4) {
+    const int mode = ntt64_mode(LOGN, fwd);
+    if (!natural && mode > 0)
+      return launch_b64<LOGN>(fwd, reinterpret_cast<const uint64_t*>(in),
+                              reinterpret_cast<uint64_t*>(out), batch, nprimes, prime_base,
+                              reinterpret_cast<const ulonglong2*>(tw),
+                              reinterpret_cast<const Prime64Info*>(info), st, mode == 2);
   }
   if (total > 0x7fffffff) return fail("ntt: batch too large");
   if (fwd) {
@@ -425,12 +563,241 @@ __global__ void k_permute_bitrev64(const uint64_t* __restrict__ in, uint64_t* __
 
 }  // namespace hefv
 
+// ---------------------------------------------------------------------------
+// 64-bit primes, N in {2^15, 2^16}: one thread-block CLUSTER per polynomial.
+// CL = N / 2^14 CTAs of 1024 threads x 16 words; each CTA owns a 2^14-word
+// tile (139 KB) of the polynomial.  The transform is the single-CTA one
+// (ntt.cuh) run over the cluster's CL*1024 threads ("gtid"): its first
+// radix-16 pass spans the whole polynomial, so exchange 0 goes through
+// distributed shared memory (st.shared::cluster into the owner CTA's tile,
+// bracketed by cluster barriers); every later pass and exchange stays inside
+// one CTA's contiguous 2^14-word block, exactly as in the 2^14 transform.
+// One HBM read and one HBM write per polynomial (the radix-pass fallback
+// below makes four round trips).  Same twiddle tables and butterflies, so
+// the limbs are identical to the other paths.
+// ---------------------------------------------------------------------------
+namespace hefv {
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile(
+      "barrier.cluster.arrive.release.aligned;\n"
+      "barrier.cluster.wait.acquire.aligned;" ::
+          : "memory");
+}
+__device__ __forceinline__ uint32_t dsmem_map(uint32_t local_addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void dsmem_st64(uint32_t addr, uint64_t v) {
+  asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+}
+
+template <int LOGN>
+struct Cl64 {
+  static constexpr int CL = 1 << (LOGN - 14);  // CTAs per cluster
+  static constexpr int LOCAL = 1 << 14;        // words per CTA tile
+  // every exchange pads with ratio 1/16 (xpad_k / xpad_s), so a CTA's block
+  // [r LOCAL, (r+1) LOCAL) starts at padded address r * LP
+  static constexpr int LP = LOCAL + LOCAL / 16;
+  static constexpr size_t smem = (size_t)((spad_size(LOCAL) + 1) & ~1) * 8;
+};
+
+template <int LOGN>
+__global__ void __cluster_dims__(1 << (LOGN - 14), 1, 1) __launch_bounds__(1024, 1)
+    k_ntt64_cl_fwd(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, int nprimes,
+                   int prime_base, const ulonglong2* __restrict__ tw_all,
+                   const Prime64Info* __restrict__ info) {
+  typedef Geo<LOGN, 4> G_;
+  typedef Cl64<LOGN> C_;
+  constexpr int E = 16, NT = G_::NT, LP = C_::LP;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  uint64_t* sm = reinterpret_cast<uint64_t*>(smraw);
+  const int tid = threadIdx.x;
+  const int r = (int)cluster_ctarank();
+  const int gtid = r * 1024 + tid;
+  const size_t poly = blockIdx.x / C_::CL;
+  const int pi = prime_base + (int)(poly % nprimes);
+  const uint64_t p = info[pi].p;
+  const Mod64 md{p, 2 * p};
+  const ulonglong2* tw = tw_all + (size_t)pi * G_::N;
+  const uint64_t* src = in + poly * G_::N;
+  uint64_t* dst = out + poly * G_::N;
+  uint64_t x[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const uint64_t v = src[gtid + e * NT];
+    x[e] = v >= p ? barrett64(v, p, info[pi].mu) : v;
+  }
+  fwd_full_pass<LOGN, 4, Mod64>(md, x, 0, gtid, tw);
+  cluster_sync_all();  // every CTA of the cluster is running (its tile may be written)
+  {
+    constexpr int K = xpad_k(LOGN, 4, 0), S = xpad_s(LOGN, 4, 0);
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(sm);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int owner = e / (E / C_::CL);  // element gtid + e NT lives in block `owner`
+      const int a = xaddr_full<LOGN, 4>(0, gtid, e, K, S) - owner * LP;
+      dsmem_st64(dsmem_map(base + 8u * (uint32_t)a, (uint32_t)owner), x[e]);
+    }
+    cluster_sync_all();
+#pragma unroll
+    for (int e = 0; e < E; ++e) x[e] = sm[xaddr_full<LOGN, 4>(1, gtid, e, K, S) - r * LP];
+  }
+#pragma unroll
+  for (int pass = 1; pass < G_::NFULL; ++pass) {
+    fwd_full_pass<LOGN, 4, Mod64>(md, x, pass, gtid, tw);
+    group_sync<10>(tid, LOGN - (pass + 1) * 4);
+    const int K = xpad_k(LOGN, 4, pass), S = xpad_s(LOGN, 4, pass);
+#pragma unroll
+    for (int e = 0; e < E; ++e) sm[xaddr_full<LOGN, 4>(pass, gtid, e, K, S) - r * LP] = x[e];
+    group_sync<10>(tid, LOGN - (pass + 1) * 4);
+    if (pass + 1 < G_::NFULL) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) x[e] = sm[xaddr_full<LOGN, 4>(pass + 1, gtid, e, K, S) - r * LP];
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) x[e] = sm[xaddr_row<LOGN, 4>(gtid, e, K, S) - r * LP];
+    }
+  }
+  fwd_last_pass<LOGN, 4, Mod64>(md, x, gtid, tw);
+#pragma unroll
+  for (int e = 0; e < E; ++e) x[e] = md.canon4(x[e]);
+  store_row_vec<LOGN, 4, uint64_t>(dst, gtid, x);
+}
+
+template <int LOGN>
+__global__ void __cluster_dims__(1 << (LOGN - 14), 1, 1) __launch_bounds__(1024, 1)
+    k_ntt64_cl_inv(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, int nprimes,
+                   int prime_base, const ulonglong2* __restrict__ itw_all,
+                   const Prime64Info* __restrict__ info) {
+  typedef Geo<LOGN, 4> G_;
+  typedef Cl64<LOGN> C_;
+  constexpr int E = 16, NT = G_::NT, LP = C_::LP;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  uint64_t* sm = reinterpret_cast<uint64_t*>(smraw);
+  const int tid = threadIdx.x;
+  const int r = (int)cluster_ctarank();
+  const int gtid = r * 1024 + tid;
+  const size_t poly = blockIdx.x / C_::CL;
+  const int pi = prime_base + (int)(poly % nprimes);
+  const Prime64Info* ip = info + pi;
+  const uint64_t p = ip->p;
+  const Mod64 md{p, 2 * p};
+  const ulonglong2* itw = itw_all + (size_t)pi * G_::N;
+  const uint64_t* src = in + poly * G_::N;
+  uint64_t* dst = out + poly * G_::N;
+  uint64_t x[E];
+  load_row_vec<LOGN, 4, uint64_t>(src, gtid, x);
+  inv_last_pass<LOGN, 4, Mod64>(md, x, gtid, itw, ip->ninv, ip->wn);
+#pragma unroll
+  for (int pass = G_::NFULL - 1; pass >= 1; --pass) {
+    const int K = xpad_k(LOGN, 4, pass), S = xpad_s(LOGN, 4, pass);
+    if (pass == G_::NFULL - 1) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) sm[xaddr_row<LOGN, 4>(gtid, e, K, S) - r * LP] = x[e];
+    } else {
+      group_sync<10>(tid, LOGN - (pass + 2) * 4);
+#pragma unroll
+      for (int e = 0; e < E; ++e) sm[xaddr_full<LOGN, 4>(pass + 1, gtid, e, K, S) - r * LP] = x[e];
+    }
+    group_sync<10>(tid, LOGN - (pass + 1) * 4);
+#pragma unroll
+    for (int e = 0; e < E; ++e) x[e] = sm[xaddr_full<LOGN, 4>(pass, gtid, e, K, S) - r * LP];
+    inv_full_pass<LOGN, 4, Mod64>(md, x, pass, gtid, itw, ip->ninv, ip->wn);
+  }
+  // exchange 0 (pass-1 layout -> pass-0 layout) through DSMEM: element i goes
+  // to the CTA whose threads read it in pass 0, r' = (i mod NT) / 1024, at the
+  // local index (i mod 1024) + (i / NT) * 1024 of that CTA's tile
+  cluster_sync_all();  // every CTA has finished reading its own tile
+  {
+    constexpr int K = xpad_k(LOGN, 4, 0), S = xpad_s(LOGN, 4, 0);
+    constexpr int TSH1 = LOGN - 8;
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(sm);
+    const int G1 = gtid >> TSH1, L1 = gtid & ((1 << TSH1) - 1);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = (G1 << (LOGN - 4)) + L1 + (e << TSH1);
+      const int owner = (i & (NT - 1)) >> 10;
+      const int li = (i & 1023) + ((i >> (LOGN - 4)) << 10);
+      dsmem_st64(dsmem_map(base + 8u * (uint32_t)(li + K * (li >> S)), (uint32_t)owner), x[e]);
+    }
+    cluster_sync_all();
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int li = tid + (e << 10);
+      x[e] = sm[li + K * (li >> S)];
+    }
+  }
+  inv_full_pass<LOGN, 4, Mod64>(md, x, 0, gtid, itw, ip->ninv, ip->wn);
+#pragma unroll
+  for (int e = 0; e < E; ++e) dst[gtid + e * NT] = md.subp(x[e]);
+}
+
+template <int LOGN>
+static int launch_cl64(bool fwd, const uint64_t* in, uint64_t* out, int64_t total_polys,
+                       int nprimes, int prime_base, const ulonglong2* tw,
+                       const Prime64Info* info, cudaStream_t st) {
+  typedef Cl64<LOGN> C_;
+  auto kern = fwd ? k_ntt64_cl_fwd<LOGN> : k_ntt64_cl_inv<LOGN>;
+  HEFV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C_::smem));
+  if (total_polys * C_::CL > 0x7fffffff) return fail("ntt64: batch too large");
+  kern<<<(unsigned)(total_polys * C_::CL), 1024, C_::smem, st>>>(in, out, nprimes, prime_base, tw,
+                                                                 info);
+  HEFV_LAUNCH_CHECK("k_ntt64_cl");
+  return 0;
+}
+
+static bool ntt64_cluster_enabled() {
+  static int m = -1;
+  if (m < 0) {
+    const char* v = std::getenv("HEFV_NTT64_CLUSTER");
+    m = v ? std::atoi(v) : 1;
+  }
+  return m != 0;
+}
+
+}  // namespace hefv
+
 int hefv_ntt64_large(hefv_ctx* c, bool fwd, const uint64_t* in, uint64_t* out, int64_t batch,
                      int nprimes, int prime_base, int natural, cudaStream_t st) {
   const int log_n = c->log_n;
   const int64_t n = c->n;
   const int64_t total_polys = batch * nprimes;
   if (total_polys <= 0) return 0;
+  if ((log_n == 15 || log_n == 16) && ntt64_cluster_enabled()) {
+    auto run = [&](const uint64_t* a, uint64_t* b) {
+      const ulonglong2* tw = fwd ? c->d_tw64 : c->d_itw64;
+      return log_n == 15
+                 ? launch_cl64<15>(fwd, a, b, total_polys, nprimes, prime_base, tw, c->d_info64, st)
+                 : launch_cl64<16>(fwd, a, b, total_polys, nprimes, prime_base, tw, c->d_info64, st);
+    };
+    const int64_t tot = total_polys * n;
+    if (!natural) return run(in, out);
+    if (fwd) {
+      // device order into out, then permute into natural order through a temporary
+      int rc = run(in, out);
+      if (rc) return rc;
+      uint64_t* tmp = nullptr;
+      HEFV_CUDA(cudaMallocAsync(&tmp, tot * 8, st));
+      k_permute_bitrev64<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(out, tmp, log_n, tot);
+      HEFV_LAUNCH_CHECK("ntt64 permute");
+      HEFV_CUDA(cudaMemcpyAsync(out, tmp, tot * 8, cudaMemcpyDeviceToDevice, st));
+      HEFV_CUDA(cudaFreeAsync(tmp, st));
+      return 0;
+    }
+    // natural -> device order into out, then the inverse in place (every CTA
+    // of a cluster loads its input before the first cluster barrier and
+    // stores only after the last one)
+    k_permute_bitrev64<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(in, out, log_n, tot);
+    HEFV_LAUNCH_CHECK("ntt64 permute");
+    return run(out, out);
+  }
   // radix-16 passes: stages in groups of 4 (log_n = 15 -> 4,4,4,3; 16 -> 4,4,4,4)
   const int64_t blocks16 = n / 16;
   const int threads = 256;

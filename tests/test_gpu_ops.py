@@ -224,7 +224,8 @@ def test_ntt_golden_vectors(case):
 
 # ---------------------------------------------------------------- race stress
 @pytest.mark.parametrize("log_n,bits", [(10, 30), (12, 30), (13, 30), (14, 30), (15, 30),
-                                        (12, 50), (14, 55)])
+                                        (10, 50), (12, 50), (13, 60), (14, 55), (15, 55),
+                                        (16, 60)])
 def test_transform_roundtrip_stress(log_n, bits):
     """Many CTAs, repeated: device-order forward then inverse must be the
     identity bit for bit (catches exchange/barrier races)."""
@@ -261,6 +262,51 @@ def test_transform_roundtrip_stress(log_n, bits):
         nat.check(fwd(h, x.data_ptr(), y.data_ptr(), 64, 4, 0, 0, st))
         nat.check(inv(h, y.data_ptr(), z.data_ptr(), 64, 4, 0, 0, st))
         assert torch.equal(z, x)
+    lib.hefv_ctx_destroy(h)
+
+
+@pytest.mark.parametrize("log_n,bits", [(10, 50), (12, 50), (13, 60), (14, 60), (12, 20),
+                                        (15, 55), (16, 60)])
+def test_ntt64_device_order_matches_oracle(log_n, bits):
+    """Batched 64-bit device-order transforms (the persistent k_ntt64_b path,
+    several primes per CTA range, inputs up to 2^64 - 1) equal the oracle's
+    natural-order NTT of x mod p permuted into bit-reversed order, and the
+    inverse maps them back to x mod p."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1901_10074_b200 import _native as nat
+    from paper_1901_10074_b200.ring import root_of_unity
+
+    n = 1 << log_n
+    L, B = (3, 5) if log_n <= 14 else (2, 3)
+    primes = O.ntt_primes(L, bits, 2 * n)
+    psis = [root_of_unity(p, n) for p in primes]
+    lib = nat.load()
+    h = C.c_void_p()
+    nat.check(lib.hefv_ctx_create(C.byref(h), log_n, 0, None, None, L,
+                                  (C.c_uint64 * L)(*primes), (C.c_uint64 * L)(*psis)))
+    g = np.random.default_rng(log_n * 100 + bits)
+    xs = g.integers(0, 1 << 63, (B, L, n), dtype=np.uint64) * np.uint64(2) + g.integers(
+        0, 2, (B, L, n), dtype=np.uint64)
+    xs[0, 0, :4] = [0, 2**64 - 1, primes[0], primes[0] - 1]
+    x = torch.from_numpy(xs.view(np.int64)).cuda()
+    y = torch.empty_like(x)
+    z = torch.empty_like(x)
+    st = torch.cuda.current_stream().cuda_stream
+    nat.check(lib.hefv_ntt_fwd64(h, x.data_ptr(), y.data_ptr(), B, L, 0, 0, st))
+    nat.check(lib.hefv_ntt_inv64(h, y.data_ptr(), z.data_ptr(), B, L, 0, 0, st))
+    got = y.cpu().numpy().view(np.uint64)
+    back = z.cpu().numpy().view(np.uint64)
+    rev = np.array([int(format(i, f"0{log_n}b")[::-1], 2) for i in range(n)])
+    for j, p in enumerate(primes):
+        ref = O.OracleNtt(p, n)
+        for b in (0, B - 1):
+            red = np.array([int(v) % p for v in xs[b, j]], dtype=object)
+            want = np.asarray(ref.fwd(red), dtype=object)[rev]
+            assert np.array_equal(got[b, j].astype(object), want), (b, j)
+            assert np.array_equal(back[b, j].astype(object), red), (b, j)
     lib.hefv_ctx_destroy(h)
 
 
