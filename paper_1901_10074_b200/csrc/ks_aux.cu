@@ -155,7 +155,10 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
 // CTA = (aux prime t, 32-point tile m); warp w = target prime j, lane =
 // point.  Each thread keeps its point's body and mask key words of every
 // digit in registers (2K words).
-constexpr int KSA_STAGES = 4;
+#ifndef KSA_STAGES_V
+#define KSA_STAGES_V 4
+#endif
+constexpr int KSA_STAGES = KSA_STAGES_V;  // depth of the digit-tile ring
 
 __device__ __forceinline__ void mad_wide(uint64_t& acc, uint32_t a, uint32_t b) {
   asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc) : "r"(a), "r"(b));
@@ -194,10 +197,32 @@ struct Redc {
 // K: digits per point (compile time, even; ring rows k..K-1 are zeroed once
 // and their key words are zero, so padded pairs contribute nothing).
 // Warps 0..JW-1 consume (warp w = target prime j = blockIdx.z * JW + w when
-// j < k), warp JW computes the x-pair sums, warp JW+1 streams each
-// ciphertext's k x 32-word digit tile
-// with one bulk copy into a KSA_STAGES-deep ring (full / xready / empty
-// mbarriers, no CTA-wide barrier in the loop).
+// j < k), warp JW+1 streams each ciphertext's k x 32-word digit tile with one
+// bulk copy into a KSA_STAGES-deep ring, and warp JW turns every ring tile
+// into (a) the x-pair sums and (b) an interleaved copy xx[u][lane] =
+// (x_2u, x_2u+1), so a consumer loads each packed pair with one 64-bit
+// shared load.  Barriers (no CTA-wide barrier in the loop): full / empty
+// between producer and pair warp (ring), xready / xempty between the pair
+// warp and the consumers (xx).  Shared addresses of the barriers are
+// computed once (the generic -> shared conversion is not free per use).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbw(uint32_t a, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void mba(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+
 template <int K, int JW>
 __global__ void __launch_bounds__(32 * (JW + 2), 1)
     k_ksa_mac(const uint32_t* __restrict__ X, const uint32_t* __restrict__ kaux,
@@ -205,9 +230,11 @@ __global__ void __launch_bounds__(32 * (JW + 2), 1)
               const Prime32Info* __restrict__ info) {
   static_assert(K % 2 == 0, "digit pairs");
   constexpr int H = K / 2;
-  __shared__ __align__(128) uint32_t ring[KSA_STAGES][K * 32];
-  __shared__ __align__(16) uint64_t xpair[KSA_STAGES][32];
-  __shared__ __align__(8) uint64_t full[KSA_STAGES], xready[KSA_STAGES], empty[KSA_STAGES];
+  constexpr int S = KSA_STAGES;
+  __shared__ __align__(128) uint32_t ring[S][K * 32];
+  __shared__ __align__(16) uint2 xx[S][H][32];
+  __shared__ __align__(16) uint64_t xpair[S][32];
+  __shared__ __align__(8) uint64_t bars[4][S];  // full, empty, xready, xempty
   const int n = 1 << log_n;
   const int tiles = n >> 5;
   const int t = blockIdx.x / tiles;
@@ -217,44 +244,52 @@ __global__ void __launch_bounds__(32 * (JW + 2), 1)
   const int64_t bbeg = (int64_t)blockIdx.y * KSA_MAC_CTS;
   const int64_t bend = min(B, bbeg + KSA_MAC_CTS);
   const int nb = (int)(bend - bbeg);
-  const uint32_t tile_bytes = (uint32_t)k * 32 * 4;
-  // X tile of ciphertext b: (((b * 3 + t) * tiles + m) * k) * 32 words, k*32 long
-  const size_t xstride = (size_t)3 * tiles * k * 32;
-  const uint32_t* xsrc = X + (((size_t)bbeg * 3 + t) * tiles + m) * k * 32;
+  const uint32_t full0 = smem_u32(&bars[0][0]), empty0 = smem_u32(&bars[1][0]);
+  const uint32_t xready0 = smem_u32(&bars[2][0]), xempty0 = smem_u32(&bars[3][0]);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < KSA_STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&xready[s], 1);
-      mbar_init(&empty[s], JW + 1);
+    for (int st = 0; st < S; ++st) {
+      mbar_init(&bars[0][st], 1);
+      mbar_init(&bars[1][st], 1);
+      mbar_init(&bars[2][st], 1);
+      mbar_init(&bars[3][st], JW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int q = k * 32 + threadIdx.x; q < K * 32; q += blockDim.x)
-    for (int s = 0; s < KSA_STAGES; ++s) ring[s][q] = 0u;
+    for (int st = 0; st < S; ++st) ring[st][q] = 0u;
   __syncthreads();
   if (w == JW + 1) {  // producer
     if (lane == 0) {
+      const uint32_t tile_bytes = (uint32_t)k * 32 * 4;
+      // X tile of ciphertext b: (((b * 3 + t) * tiles + m) * k) * 32 words, k*32 long
+      const size_t xstride = (size_t)3 * tiles * k * 32;
+      const uint32_t* xsrc = X + (((size_t)bbeg * 3 + t) * tiles + m) * k * 32;
       for (int r = 0; r < nb; ++r) {
-        const int s = r % KSA_STAGES;
-        if (r >= KSA_STAGES) mbar_wait(&empty[s], (uint32_t)((r / KSA_STAGES - 1) & 1));
-        bulk_g2s(ring[s], xsrc + (size_t)r * xstride, tile_bytes, &full[s]);
+        const int st = r % S;
+        if (r >= S) mbw(empty0 + 8 * st, (uint32_t)((r / S - 1) & 1));
+        bulk_g2s(ring[st], xsrc + (size_t)r * xstride, tile_bytes, &bars[0][st]);
       }
     }
     return;
   }
-  if (w == JW) {  // x-pair sums
+  if (w == JW) {  // pair warp: x-pair sums + interleaved pairs
     for (int r = 0; r < nb; ++r) {
-      const int s = r % KSA_STAGES;
-      mbar_wait(&full[s], (uint32_t)((r / KSA_STAGES) & 1));
-      const uint32_t* xt = ring[s] + lane;
+      const int st = r % S;
+      mbw(full0 + 8 * st, (uint32_t)((r / S) & 1));
+      if (r >= S) mbw(xempty0 + 8 * st, (uint32_t)((r / S - 1) & 1));
+      const uint32_t* xt = ring[st] + lane;
       uint64_t p0 = 0, p1 = 0;
 #pragma unroll
-      for (int u = 0; u < H; ++u) mad_wide((u & 1) ? p1 : p0, xt[64 * u], xt[64 * u + 32]);
-      xpair[s][lane] = p0 + p1;
+      for (int u = 0; u < H; ++u) {
+        const uint32_t x0 = xt[64 * u], x1 = xt[64 * u + 32];
+        mad_wide((u & 1) ? p1 : p0, x0, x1);
+        xx[st][u][lane] = make_uint2(x0, x1);
+      }
+      xpair[st][lane] = p0 + p1;
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(&xready[s]);
-        mbar_arrive(&empty[s]);
+        mba(empty0 + 8 * st);
+        mba(xready0 + 8 * st);
       }
     }
     return;
@@ -293,23 +328,22 @@ __global__ void __launch_bounds__(32 * (JW + 2), 1)
   const size_t ymask = (size_t)k * n;
   const size_t ystride = (size_t)3 * 2 * k * n;
   for (int r = 0; r < nb; ++r) {
-    const int s = r % KSA_STAGES;
-    const uint32_t ph = (uint32_t)((r / KSA_STAGES) & 1);
-    mbar_wait(&full[s], ph);
-    const uint32_t* xt = ring[s] + lane;
+    const int st = r % S;
+    mbw(xready0 + 8 * st, (uint32_t)((r / S) & 1));
+    const uint2* xs = &xx[st][0][lane];
     uint64_t b0 = 0, b1 = 0, m0 = 0, m1 = 0;
 #pragma unroll
     for (int u = 0; u < H; ++u) {
       // (x_2u+1 : x_2u) + (k_2u : k_2u+1) = (x_2u+1 + k_2u : x_2u + k_2u+1)
-      const uint64_t xx = ((uint64_t)xt[64 * u + 32] << 32) | xt[64 * u];
-      const uint64_t sb = xx + kb[u], sm = xx + km[u];
+      const uint2 xv = xs[32 * u];
+      const uint64_t xw = ((uint64_t)xv.y << 32) | xv.x;
+      const uint64_t sb = xw + kb[u], sm = xw + km[u];
       mad_wide((u & 1) ? b1 : b0, (uint32_t)sb, (uint32_t)(sb >> 32));
       mad_wide((u & 1) ? m1 : m0, (uint32_t)sm, (uint32_t)(sm >> 32));
     }
-    mbar_wait(&xready[s], ph);
-    const uint64_t xp = xpair[s][lane];
+    const uint64_t xp = xpair[st][lane];
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    if (lane == 0) mba(xempty0 + 8 * st);
     if (active) {
       yb[0] = red(b0 + b1 - xp - kpb);
       yb[ymask] = red(m0 + m1 - xp - kpm);
@@ -370,7 +404,10 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
       const Mod32 ma{pa.p, 2 * pa.p};
       mbar_wait(mbar, phase);
       phase ^= 1u;
-      load_row_vec<LOGN, LOGE>(stage, tid, x);
+      if constexpr (LOGE == 4)
+        load_row16_smem(stage, tid, x);
+      else
+        load_row_vec<LOGN, LOGE>(stage, tid, x);
       const uint32_t* nxt = t < 2 ? row(b, t + 1) : (b + 1 < bend ? row(b + 1, 0) : nullptr);
       auto hook = [&]() {
         if (tid == 0 && nxt) bulk_g2s(stage, nxt, N * 4, mbar);

@@ -486,4 +486,34 @@ __device__ __forceinline__ void load_row_vec(const T* __restrict__ base, int tid
   }
 }
 
+// Row-layout read of 16 consecutive 32-bit words per thread from SHARED
+// memory (a bulk-copied staging row) without bank conflicts: plain 128-bit
+// loads at a 64-byte lane stride serve 2 lanes per wavefront (4x the
+// wavefronts); here lane L loads its quads rotated by r = (L >> 1) & 3, so
+// every 8 lanes of an instruction hit 8 distinct 16-byte bank groups, and the
+// registers are un-rotated with two conditional quad shifts (32 SELs).
+__device__ __forceinline__ void load_row16_smem(const uint32_t* base, int tid, uint32_t* x) {
+  const int rot = (tid >> 1) & 3;
+  const uint4* p = reinterpret_cast<const uint4*>(base + (tid << 4));
+  uint4 v[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) v[q] = p[(q + rot) & 3];  // v[q] = quad (q + rot) & 3
+  // quad qq = v[(qq - rot) & 3]: rotate right by rot & 1, then by rot & 2
+  const bool r1 = rot & 1, r2 = rot & 2;
+  uint4 w[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint4 a = v[q], b = v[(q + 3) & 3];
+    w[q] = make_uint4(r1 ? b.x : a.x, r1 ? b.y : a.y, r1 ? b.z : a.z, r1 ? b.w : a.w);
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint4 a = w[q], b = w[(q + 2) & 3];
+    x[4 * q + 0] = r2 ? b.x : a.x;
+    x[4 * q + 1] = r2 ? b.y : a.y;
+    x[4 * q + 2] = r2 ? b.z : a.z;
+    x[4 * q + 3] = r2 ? b.w : a.w;
+  }
+}
+
 }  // namespace hefv

@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(Geo<LOGN, 4>::NT, 1024 / Geo<LOGN, 4>::NT)
       for (int e = 0; e < E; ++e) x[e] = md.canon4(x[e]);
       store_row_vec<LOGN, 4, uint32_t>(out + poly(q), tid, x);
     } else {
-      load_row_vec<LOGN, 4, uint32_t>(stage, tid, x);
+      load_row16_smem(stage, tid, x);
       cta_inv<LOGN, 4, Mod32>(md, x, sm, tws, inf.ninv, inf.wn, twg, hook);
       uint32_t* dst = out + poly(q);
 #pragma unroll
