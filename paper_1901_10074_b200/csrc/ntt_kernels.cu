@@ -20,7 +20,7 @@ template <int LOGN, int LOGE, class M>
 __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT)
     k_ntt_fwd(const typename M::T* __restrict__ in, typename M::T* __restrict__ out, int nprimes,
               int prime_base, int natural, const typename M::Tw* __restrict__ tw_all,
-              const typename InfoOf<M>::I* __restrict__ info) {
+              const typename InfoOf<M>::I* __restrict__ info, int bcast) {
   typedef Geo<LOGN, LOGE> G_;
   typedef typename M::T T;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -30,7 +30,8 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT)
   const auto inf = info[pi];
   const M md = make_mod(inf);
   const typename M::Tw* tw = tw_all + (size_t)pi * G_::N;
-  const T* src = in + poly * G_::N;
+  // bcast: one input row per batch index, transformed under every prime
+  const T* src = in + (bcast ? poly / nprimes : poly) * G_::N;
   T* dst = out + poly * G_::N;
   const int tid = threadIdx.x;
   T x[G_::E];
@@ -95,13 +96,6 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT)
 // bulk-copied (cp.async.bulk) into a staging buffer one transform ahead (the
 // copy is issued right after the current transform's first CTA barrier).
 
-// x < 2^32 -> [0, 4p), the lazy forward transform's input range
-__device__ __forceinline__ uint32_t to_lazy4(uint32_t x, const Prime32Info& inf) {
-  if (inf.p >= (1u << 30)) return x;
-  if (inf.p > (1u << 29)) return x >= 4 * inf.p ? x - 4 * inf.p : x;
-  return barrett62(x, inf.p, inf.mu);
-}
-
 template <int LOGN, bool FWD>
 __global__ void __launch_bounds__(Geo<LOGN, 4>::NT, 1024 / Geo<LOGN, 4>::NT)
     k_ntt32_b(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int64_t batch,
@@ -158,8 +152,22 @@ __global__ void __launch_bounds__(Geo<LOGN, 4>::NT, 1024 / Geo<LOGN, 4>::NT)
       if (tid == 0 && nxt) bulk_g2s(stage, nxt, N * 4, mbar);
     };
     if constexpr (FWD) {
+      // input -> [0, 4p): the prime's class is uniform, so branch once around
+      // the 16 loads (a per-element branch costs ~8 issue slots per word)
+      if (inf.p >= (1u << 30)) {
 #pragma unroll
-      for (int e = 0; e < E; ++e) x[e] = to_lazy4(stage[tid + e * NT], inf);
+        for (int e = 0; e < E; ++e) x[e] = stage[tid + e * NT];
+      } else if (inf.p > (1u << 29)) {
+        const uint32_t p4 = 4 * inf.p;  // x < 2^32 < 8p: one conditional subtraction
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const uint32_t v = stage[tid + e * NT];
+          x[e] = min(v, v - p4);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) x[e] = barrett62(stage[tid + e * NT], inf.p, inf.mu);
+      }
       cta_fwd<LOGN, 4, Mod32>(md, x, sm, tws, twg, hook, LOGN - G_::RLAST);
 #pragma unroll
       for (int e = 0; e < E; ++e) x[e] = md.canon4(x[e]);
@@ -199,7 +207,7 @@ template <int LOGN, bool FWD, bool STAGE>
 __global__ void __launch_bounds__(Geo<LOGN, 4>::NT, LOGN >= 13 ? 1024 / Geo<LOGN, 4>::NT : 2)
     k_ntt64_b(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, int64_t batch,
               int nprimes, int prime_base, const ulonglong2* __restrict__ tw_all,
-              const Prime64Info* __restrict__ info) {
+              const Prime64Info* __restrict__ info, int bcast) {
   typedef Geo<LOGN, 4> G_;
   constexpr int E = G_::E;
   constexpr int NT = G_::NT;
@@ -236,11 +244,12 @@ __global__ void __launch_bounds__(Geo<LOGN, 4>::NT, LOGN >= 13 ? 1024 / Geo<LOGN
         __syncthreads();
       }
     }
-    const uint64_t* src = in + b * pstride + (int64_t)j * N;
+    const uint64_t* src = bcast ? in + b * N : in + b * pstride + (int64_t)j * N;
     uint64_t* dst = out + b * pstride + (int64_t)j * N;
     if (tid == 0 && q + 1 < qend) {
       const bool wrap = b + 1 == batch;
-      bulk_prefetch_l2(wrap ? in + (j + 1) * (int64_t)N : src + pstride, N * 8);
+      bulk_prefetch_l2(bcast ? (wrap ? in : src + N)
+                             : (wrap ? in + (j + 1) * (int64_t)N : src + pstride), N * 8);
     }
     ++b;
     const Mod64 md{p, 2 * p};
@@ -315,7 +324,7 @@ static int ntt64_mode(int log_n, bool fwd) {
 template <int LOGN>
 static int launch_b64(bool fwd, const uint64_t* in, uint64_t* out, int64_t batch, int nprimes,
                       int prime_base, const ulonglong2* tw, const Prime64Info* info, cudaStream_t st,
-                      bool stage) {
+                      bool stage, int bcast) {
   typedef Geo<LOGN, 4> G_;
   const size_t smem = Ntt64B<LOGN>::smem(stage);
   auto kern = fwd ? (stage ? k_ntt64_b<LOGN, true, true> : k_ntt64_b<LOGN, true, false>)
@@ -328,7 +337,7 @@ static int launch_b64(bool fwd, const uint64_t* in, uint64_t* out, int64_t batch
   const int64_t P = batch * nprimes;
   const int64_t slots = (int64_t)sm_count() * per_sm;
   const unsigned grid = (unsigned)(P < slots ? P : slots);
-  kern<<<grid, G_::NT, smem, st>>>(in, out, batch, nprimes, prime_base, tw, info);
+  kern<<<grid, G_::NT, smem, st>>>(in, out, batch, nprimes, prime_base, tw, info, bcast);
   HEFV_LAUNCH_CHECK("k_ntt64_b");
   return 0;
 }
@@ -336,14 +345,14 @@ static int launch_b64(bool fwd, const uint64_t* in, uint64_t* out, int64_t batch
 template <int LOGN, int LOGE, class M>
 static int launch_one(bool fwd, const typename M::T* in, typename M::T* out, int64_t batch,
                       int nprimes, int prime_base, int natural, const typename M::Tw* tw,
-                      const typename InfoOf<M>::I* info, cudaStream_t st) {
+                      const typename InfoOf<M>::I* info, cudaStream_t st, int bcast) {
   typedef Geo<LOGN, LOGE> G_;
   const size_t smem = (size_t)spad_size(G_::N) * sizeof(typename M::T);
   const int64_t total = batch * nprimes;
   if (total <= 0) return 0;
   if constexpr (sizeof(typename M::T) == 4 && LOGN >= 10 && LOGN <= 14 && LOGE == 4) {
     // twiddles of the 32-bit set: fwd and inverse tables have the same type
-    if (!natural)
+    if (!natural && !bcast)
       return launch_b32<LOGN>(fwd, reinterpret_cast<const uint32_t*>(in),
                               reinterpret_cast<uint32_t*>(out), batch, nprimes, prime_base,
                               reinterpret_cast<const uint2*>(tw),
@@ -355,13 +364,14 @@ static int launch_one(bool fwd, const typename M::T* in, typename M::T* out, int
       return launch_b64<LOGN>(fwd, reinterpret_cast<const uint64_t*>(in),
                               reinterpret_cast<uint64_t*>(out), batch, nprimes, prime_base,
                               reinterpret_cast<const ulonglong2*>(tw),
-                              reinterpret_cast<const Prime64Info*>(info), st, mode == 2);
+                              reinterpret_cast<const Prime64Info*>(info), st, mode == 2, bcast);
   }
   if (total > 0x7fffffff) return fail("ntt: batch too large");
   if (fwd) {
     auto kern = k_ntt_fwd<LOGN, LOGE, M>;
     HEFV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(unsigned)total, G_::NT, smem, st>>>(in, out, nprimes, prime_base, natural, tw, info);
+    kern<<<(unsigned)total, G_::NT, smem, st>>>(in, out, nprimes, prime_base, natural, tw, info,
+                                                bcast);
   } else {
     auto kern = k_ntt_inv<LOGN, LOGE, M>;
     HEFV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -374,17 +384,18 @@ static int launch_one(bool fwd, const typename M::T* in, typename M::T* out, int
 template <class M>
 static int dispatch(int log_n, bool fwd, const typename M::T* in, typename M::T* out,
                     int64_t batch, int nprimes, int prime_base, int natural,
-                    const typename M::Tw* tw, const typename InfoOf<M>::I* info, cudaStream_t st) {
+                    const typename M::Tw* tw, const typename InfoOf<M>::I* info, cudaStream_t st,
+                    int bcast = 0) {
 #define HEFV_CASE(L) \
   case L:            \
-    return launch_one<L, 4, M>(fwd, in, out, batch, nprimes, prime_base, natural, tw, info, st);
+    return launch_one<L, 4, M>(fwd, in, out, batch, nprimes, prime_base, natural, tw, info, st, bcast);
   switch (log_n) {
     case 1:
-      return launch_one<1, 1, M>(fwd, in, out, batch, nprimes, prime_base, natural, tw, info, st);
+      return launch_one<1, 1, M>(fwd, in, out, batch, nprimes, prime_base, natural, tw, info, st, bcast);
     case 2:
-      return launch_one<2, 2, M>(fwd, in, out, batch, nprimes, prime_base, natural, tw, info, st);
+      return launch_one<2, 2, M>(fwd, in, out, batch, nprimes, prime_base, natural, tw, info, st, bcast);
     case 3:
-      return launch_one<3, 3, M>(fwd, in, out, batch, nprimes, prime_base, natural, tw, info, st);
+      return launch_one<3, 3, M>(fwd, in, out, batch, nprimes, prime_base, natural, tw, info, st, bcast);
     HEFV_CASE(4)
     HEFV_CASE(5)
     HEFV_CASE(6)
@@ -402,7 +413,7 @@ static int dispatch(int log_n, bool fwd, const typename M::T* in, typename M::T*
 #undef HEFV_CASE
   if constexpr (sizeof(typename M::T) == 4) {
     if (log_n == 15)
-      return launch_one<15, 5, M>(fwd, in, out, batch, nprimes, prime_base, natural, tw, info, st);
+      return launch_one<15, 5, M>(fwd, in, out, batch, nprimes, prime_base, natural, tw, info, st, bcast);
   }
   return -100;  // not handled by the CTA-resident path
 }
@@ -412,7 +423,7 @@ static int dispatch(int log_n, bool fwd, const typename M::T* in, typename M::T*
 using namespace hefv;
 
 int hefv_ntt64_large(hefv_ctx* c, bool fwd, const uint64_t* in, uint64_t* out, int64_t batch,
-                     int nprimes, int prime_base, int natural, cudaStream_t st);
+                     int nprimes, int prime_base, int natural, cudaStream_t st, int bcast = 0);
 
 extern "C" {
 
@@ -465,6 +476,18 @@ int hefv_ntt_inv64(hefv_ctx* c, const uint64_t* in, uint64_t* out, int64_t batch
 }
 
 }  // extern "C"
+
+// Forward transforms (device order) of `rows` input rows under every 64-bit
+// prime of the context: out[r][j] = NTT_j(in[r] mod p_j).  Internal (the
+// 64-bit key switch reads its digit rows this way instead of materialising
+// L reduced copies).
+int hefv_ntt64_fwd_rows(hefv_ctx* c, const uint64_t* in, uint64_t* out, int64_t rows,
+                        cudaStream_t st) {
+  int r = dispatch<Mod64>(c->log_n, true, in, out, rows, c->n64, 0, 0, c->d_tw64, c->d_info64, st,
+                          1);
+  if (r == -100) return hefv_ntt64_large(c, true, in, out, rows, c->n64, 0, 0, st, 1);
+  return r;
+}
 
 // ---------------------------------------------------------------------------
 // 64-bit primes, N in {2^15, 2^16}: two CTA-resident passes through HBM.
@@ -612,7 +635,7 @@ template <int LOGN>
 __global__ void __cluster_dims__(1 << (LOGN - 14), 1, 1) __launch_bounds__(1024, 1)
     k_ntt64_cl_fwd(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, int nprimes,
                    int prime_base, const ulonglong2* __restrict__ tw_all,
-                   const Prime64Info* __restrict__ info) {
+                   const Prime64Info* __restrict__ info, int bcast) {
   typedef Geo<LOGN, 4> G_;
   typedef Cl64<LOGN> C_;
   constexpr int E = 16, NT = G_::NT, LP = C_::LP;
@@ -626,7 +649,7 @@ __global__ void __cluster_dims__(1 << (LOGN - 14), 1, 1) __launch_bounds__(1024,
   const uint64_t p = info[pi].p;
   const Mod64 md{p, 2 * p};
   const ulonglong2* tw = tw_all + (size_t)pi * G_::N;
-  const uint64_t* src = in + poly * G_::N;
+  const uint64_t* src = in + (bcast ? poly / nprimes : poly) * G_::N;
   uint64_t* dst = out + poly * G_::N;
   uint64_t x[E];
 #pragma unroll
@@ -675,7 +698,7 @@ template <int LOGN>
 __global__ void __cluster_dims__(1 << (LOGN - 14), 1, 1) __launch_bounds__(1024, 1)
     k_ntt64_cl_inv(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, int nprimes,
                    int prime_base, const ulonglong2* __restrict__ itw_all,
-                   const Prime64Info* __restrict__ info) {
+                   const Prime64Info* __restrict__ info, int /*bcast*/) {
   typedef Geo<LOGN, 4> G_;
   typedef Cl64<LOGN> C_;
   constexpr int E = 16, NT = G_::NT, LP = C_::LP;
@@ -742,13 +765,13 @@ __global__ void __cluster_dims__(1 << (LOGN - 14), 1, 1) __launch_bounds__(1024,
 template <int LOGN>
 static int launch_cl64(bool fwd, const uint64_t* in, uint64_t* out, int64_t total_polys,
                        int nprimes, int prime_base, const ulonglong2* tw,
-                       const Prime64Info* info, cudaStream_t st) {
+                       const Prime64Info* info, cudaStream_t st, int bcast) {
   typedef Cl64<LOGN> C_;
   auto kern = fwd ? k_ntt64_cl_fwd<LOGN> : k_ntt64_cl_inv<LOGN>;
   HEFV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C_::smem));
   if (total_polys * C_::CL > 0x7fffffff) return fail("ntt64: batch too large");
   kern<<<(unsigned)(total_polys * C_::CL), 1024, C_::smem, st>>>(in, out, nprimes, prime_base, tw,
-                                                                 info);
+                                                                 info, bcast);
   HEFV_LAUNCH_CHECK("k_ntt64_cl");
   return 0;
 }
@@ -765,17 +788,21 @@ static bool ntt64_cluster_enabled() {
 }  // namespace hefv
 
 int hefv_ntt64_large(hefv_ctx* c, bool fwd, const uint64_t* in, uint64_t* out, int64_t batch,
-                     int nprimes, int prime_base, int natural, cudaStream_t st) {
+                     int nprimes, int prime_base, int natural, cudaStream_t st, int bcast) {
   const int log_n = c->log_n;
   const int64_t n = c->n;
   const int64_t total_polys = batch * nprimes;
   if (total_polys <= 0) return 0;
+  if (bcast && !((log_n == 15 || log_n == 16) && ntt64_cluster_enabled()))
+    return fail("ntt64: broadcast input rows need the cluster transform");
   if ((log_n == 15 || log_n == 16) && ntt64_cluster_enabled()) {
     auto run = [&](const uint64_t* a, uint64_t* b) {
       const ulonglong2* tw = fwd ? c->d_tw64 : c->d_itw64;
       return log_n == 15
-                 ? launch_cl64<15>(fwd, a, b, total_polys, nprimes, prime_base, tw, c->d_info64, st)
-                 : launch_cl64<16>(fwd, a, b, total_polys, nprimes, prime_base, tw, c->d_info64, st);
+                 ? launch_cl64<15>(fwd, a, b, total_polys, nprimes, prime_base, tw, c->d_info64, st,
+                                   bcast)
+                 : launch_cl64<16>(fwd, a, b, total_polys, nprimes, prime_base, tw, c->d_info64, st,
+                                   bcast);
     };
     const int64_t tot = total_polys * n;
     if (!natural) return run(in, out);
