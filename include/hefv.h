@@ -244,6 +244,21 @@ int hefv_keyswitch64(hefv_ctx* ctx, const uint64_t* kbody, const uint64_t* kmask
 int hefv_to_montgomery64(hefv_ctx* ctx, const uint64_t* in, uint64_t* out, int64_t rows,
                          void* stream);
 
+/* ---- 64-bit RNS key switch through an aux basis (same limbs as
+ * hefv_keyswitch64; fv.py:205-217) ------------------------------------------
+ * The context holds the L <= 8 64-bit primes and, as its 32-bit prime set,
+ * exactly T aux NTT primes (a_t < 2^62 / L squared-bound, prod a_t > 8 L N
+ * max(p)^2); hefv_ks64_aux_setup(ctx, T) validates and tabulates the CRT.
+ * hefv_ks64_aux_key: kbody/kmask (L, L, N) [target j][digit i], device NTT
+ * order, plain residues -> kaux (T, 2L, L, N) u32; scratch (4 + T) L L N u64.
+ * hefv_keyswitch64_aux: digits (B, L, N) coefficient limbs -> out (B, 2, L, N)
+ * coefficient domain; scratch B * 3 * L * T * N u32. */
+int hefv_ks64_aux_setup(hefv_ctx* ctx, int32_t T);
+int hefv_ks64_aux_key(hefv_ctx* ctx, const uint64_t* kbody, const uint64_t* kmask,
+                      uint32_t* kaux, uint64_t* scratch, void* stream);
+int hefv_keyswitch64_aux(hefv_ctx* ctx, const uint32_t* kaux, const uint64_t* digits,
+                         uint64_t* out, uint32_t* scratch, int64_t B, void* stream);
+
 /* ---- measurement ---------------------------------------------------------
  * Integer-pipe throughput probe (roofline denominator; not a reference
  * function): kind 0 IMAD, 1 IMAD.HI, 2 IMAD.WIDE, 3 IADD3, 4 Shoup butterfly;

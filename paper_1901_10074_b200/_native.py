@@ -57,6 +57,9 @@ _SIGS = {
     "hefv_probe_int": [_I32, _I32, _I32, _P, _P],
     "hefv_keyswitch64": [_P, _P, _P, _P, _P, _P, _I64, _P],
     "hefv_to_montgomery64": [_P, _P, _P, _I64, _P],
+    "hefv_ks64_aux_setup": [_P, _I32],
+    "hefv_ks64_aux_key": [_P, _P, _P, _P, _P, _P],
+    "hefv_keyswitch64_aux": [_P, _P, _P, _P, _P, _I64, _P],
 }
 
 EXPORTED = tuple(["hefv_last_error", "hefv_ctx_destroy", "hefv_launch_count"] + list(_SIGS))

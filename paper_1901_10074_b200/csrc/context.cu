@@ -226,6 +226,8 @@ void hefv_ctx_destroy(hefv_ctx* c) {
   cudaFree(c->d_delta);
   cudaFree(c->d_tmod);
   cudaFree(c->d_ksa_j);
+  cudaFree(c->d_ks64a_t);
+  cudaFree(c->d_ks64a_j);
   delete c;
 }
 

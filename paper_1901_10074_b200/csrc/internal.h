@@ -67,7 +67,12 @@ struct hefv_ctx {
   bool ksa_ready = false;
   int ksa_base = -1;
   hefv::KsaJ* d_ksa_j = nullptr;
-  hefv::KsaT ksa_t{};  // key switch: 0 plain, 1 TMEM mask acc (E=16), 2 both accs in TMEM (E=32)
+  hefv::KsaT ksa_t{};
+  // aux-basis 64-bit key switch (hefv_ks64_aux_setup): the T 32-bit primes of
+  // the context are its aux primes
+  int ks64a_T = 0;
+  void* d_ks64a_t = nullptr;
+  void* d_ks64a_j = nullptr;  // key switch: 0 plain, 1 TMEM mask acc (E=16), 2 both accs in TMEM (E=32)
 };
 
 namespace hefv {

@@ -13,12 +13,25 @@
 #include "ntt.cuh"
 #include "kcommon.cuh"
 #include "tmem.cuh"
+#include "cluster.cuh"
 
 namespace hefv {
 
-template <int LOGN, int LOGE, class M>
+// transform input -> lazy range: 64-bit primes any u64; 30-bit primes from
+// u32 or from u64 < 2^62 (the 64-bit key switch's digits)
+__device__ __forceinline__ uint64_t cl_in(uint64_t v, const Prime64Info& i) {
+  return v >= i.p ? barrett64(v, i.p, i.mu) : v;
+}
+__device__ __forceinline__ uint32_t cl_in(uint64_t v, const Prime32Info& i) {
+  return barrett62(v, i.p, i.mu);
+}
+__device__ __forceinline__ uint32_t cl_in(uint32_t v, const Prime32Info& i) {
+  return barrett62(v, i.p, i.mu);
+}
+
+template <int LOGN, int LOGE, class M, class TIn = typename M::T>
 __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT)
-    k_ntt_fwd(const typename M::T* __restrict__ in, typename M::T* __restrict__ out, int nprimes,
+    k_ntt_fwd(const TIn* __restrict__ in, typename M::T* __restrict__ out, int nprimes,
               int prime_base, int natural, const typename M::Tw* __restrict__ tw_all,
               const typename InfoOf<M>::I* __restrict__ info, int bcast) {
   typedef Geo<LOGN, LOGE> G_;
@@ -31,12 +44,12 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT)
   const M md = make_mod(inf);
   const typename M::Tw* tw = tw_all + (size_t)pi * G_::N;
   // bcast: one input row per batch index, transformed under every prime
-  const T* src = in + (bcast ? poly / nprimes : poly) * G_::N;
+  const TIn* src = in + (bcast ? poly / nprimes : poly) * G_::N;
   T* dst = out + poly * G_::N;
   const int tid = threadIdx.x;
   T x[G_::E];
 #pragma unroll
-  for (int e = 0; e < G_::E; ++e) x[e] = reduce_any(src[tid + e * G_::NT], inf);
+  for (int e = 0; e < G_::E; ++e) x[e] = cl_in(src[tid + e * G_::NT], inf);
   cta_fwd<LOGN, LOGE, M>(md, x, sm, tw);
 #pragma unroll
   for (int e = 0; e < G_::E; ++e) x[e] = md.canon4(x[e]);
@@ -182,6 +195,213 @@ __global__ void __launch_bounds__(Geo<LOGN, 4>::NT, 1024 / Geo<LOGN, 4>::NT)
   }
 }
 
+// ---- 30-bit, N = 2^14: one 2-CTA cluster per polynomial ---------------------
+// Experimental (HEFV_NTT32_CL=1).  The 16384-word transform of k_ntt32_b over
+// a cluster of two 512-thread CTAs (16 words per thread, 8192-word tile
+// each), so two independent transforms share every SM (two CTAs of different
+// clusters) and one CTA's barrier / exchange phase overlaps the other's
+// butterflies.  The exchange whose group spans the whole polynomial (forward:
+// exchange 0; inverse: its last) writes into the owning CTA's tile through
+// DSMEM.  Persistent: cluster c owns the polynomial range [c P / G, (c+1) P /
+// G) in prime-major order; every input half is bulk-copied one transform
+// ahead.
+template <bool FWD>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 2)
+    k_ntt32_cl(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int64_t batch,
+               int nprimes, int prime_base, const uint2* __restrict__ tw_all,
+               const Prime32Info* __restrict__ info) {
+  constexpr int LOGN = 14;
+  typedef Geo<LOGN, 4> G_;  // over the cluster: NT = 1024 global threads
+  constexpr int E = 16, NT = G_::NT, N = G_::N, HALF = N / 2;
+  constexpr int NTW = 1 << (LOGN - G_::RLAST);
+  constexpr int LP = HALF + HALF / 16;  // padded words per CTA block (ratio 1/16)
+  extern __shared__ __align__(16) unsigned char smraw[];
+  uint2* tws = reinterpret_cast<uint2*>(smraw);
+  uint32_t* sm = reinterpret_cast<uint32_t*>(tws + NTW);
+  uint32_t* stage = sm + ((LP + 4) & ~3);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(stage + HALF);
+  const int tid = threadIdx.x;
+  const int r = (int)cluster_ctarank();
+  const int gtid = r * 512 + tid;
+  const int64_t ncl = gridDim.x >> 1, cid = blockIdx.x >> 1;
+  const int64_t P = batch * nprimes;
+  const int64_t qbeg = P * cid / ncl, qend = P * (cid + 1) / ncl;
+  auto poly = [&](int64_t q) {
+    const int64_t j = q / batch, b = q - j * batch;
+    return (b * nprimes + j) * (int64_t)N;
+  };
+  // this CTA's input: forward = column layout elements e*1024 + 512r + [0,512)
+  // (16 runs of 2 KB), inverse = row layout block [r HALF, (r+1) HALF)
+  auto issue = [&](int64_t q) {
+    const uint32_t* src = in + poly(q);
+    const uint32_t m = (uint32_t)__cvta_generic_to_shared(mbar);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(m), "r"(HALF * 4)
+                 : "memory");
+    if constexpr (FWD) {
+#pragma unroll 1
+      for (int e = 0; e < E; ++e) {
+        const uint32_t d = (uint32_t)__cvta_generic_to_shared(stage + e * 512);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(d), "l"(src + e * 1024 + 512 * r), "r"(2048), "r"(m) : "memory");
+      }
+    } else {
+      const uint32_t d = (uint32_t)__cvta_generic_to_shared(stage);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+          ::"r"(d), "l"(src + r * HALF), "r"(HALF * 4), "r"(m) : "memory");
+    }
+  };
+  if (tid == 0) {
+    mbar_init(mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (qbeg < qend && tid == 0) issue(qbeg);
+  cluster_arrive();  // pairs with the first pre-exchange wait (peer started)
+  uint32_t phase = 0;
+  int cur = -1;
+  Prime32Info inf;
+  const uint2* twg = nullptr;
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(sm);
+  const uint32_t peer = dsmem_map(base, (uint32_t)(r ^ 1));
+  for (int64_t q = qbeg; q < qend; ++q) {
+    const int j = (int)(q / batch);
+    if (j != cur) {
+      cur = j;
+      inf = info[prime_base + j];
+      twg = tw_all + (size_t)(prime_base + j) * N;
+      __syncthreads();
+      const uint4* src = reinterpret_cast<const uint4*>(twg);
+      uint4* dst = reinterpret_cast<uint4*>(tws);
+      for (int i = tid; i < NTW / 2; i += 512) dst[i] = __ldg(src + i);
+      __syncthreads();
+    }
+    const Mod32 md{inf.p, 2 * inf.p};
+    mbar_wait(mbar, phase);
+    phase ^= 1u;
+    uint32_t x[E];
+    const bool more = q + 1 < qend;
+    if constexpr (FWD) {
+      if (inf.p > (1u << 29) && inf.p < (1u << 30)) {
+        const uint32_t p4 = 4 * inf.p;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const uint32_t v = stage[e * 512 + tid];
+          x[e] = min(v, v - p4);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const uint32_t v = stage[e * 512 + tid];
+          x[e] = inf.p >= (1u << 30) ? v : barrett62(v, inf.p, inf.mu);
+        }
+      }
+      fwd_full_pass<LOGN, 4, Mod32>(md, x, 0, gtid, tws);
+      cluster_wait();  // the peer is done reading its tile (previous transform)
+      {
+        constexpr int K = xpad_k(LOGN, 4, 0), S = xpad_s(LOGN, 4, 0);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int owner = e >> 3;  // element gtid + e NT lives in block e / 8
+          const int a = xaddr_full<LOGN, 4>(0, gtid, e, K, S) - owner * LP;
+          if (owner == r)
+            sm[a] = x[e];
+          else
+            dsmem_st32(peer + 4u * (uint32_t)a, x[e]);
+        }
+        cluster_sync_all();
+        if (tid == 0 && more) issue(q + 1);  // every local thread has read its stage words
+#pragma unroll
+        for (int e = 0; e < E; ++e) x[e] = sm[xaddr_full<LOGN, 4>(1, gtid, e, K, S) - r * LP];
+      }
+#pragma unroll
+      for (int pass = 1; pass < G_::NFULL; ++pass) {
+        fwd_full_pass<LOGN, 4, Mod32>(md, x, pass, gtid, tws);
+        group_sync<9>(tid, LOGN - (pass + 1) * 4);
+        const int K = xpad_k(LOGN, 4, pass), S = xpad_s(LOGN, 4, pass);
+#pragma unroll
+        for (int e = 0; e < E; ++e) sm[xaddr_full<LOGN, 4>(pass, gtid, e, K, S) - r * LP] = x[e];
+        group_sync<9>(tid, LOGN - (pass + 1) * 4);
+        if (pass + 1 < G_::NFULL) {
+#pragma unroll
+          for (int e = 0; e < E; ++e) x[e] = sm[xaddr_full<LOGN, 4>(pass + 1, gtid, e, K, S) - r * LP];
+        } else {
+#pragma unroll
+          for (int e = 0; e < E; ++e) x[e] = sm[xaddr_row<LOGN, 4>(gtid, e, K, S) - r * LP];
+        }
+      }
+      cluster_arrive();  // this CTA's tile reads of this transform are done
+      fwd_last_pass<LOGN, 4, Mod32>(md, x, gtid, twg);
+#pragma unroll
+      for (int e = 0; e < E; ++e) x[e] = md.canon4(x[e]);
+      store_row_vec<LOGN, 4, uint32_t>(out + poly(q), gtid, x);
+    } else {
+      load_row16_smem(stage, tid, x);
+      __syncthreads();  // stage consumed; the previous transform's tile reads are done
+      if (tid == 0 && more) issue(q + 1);
+      inv_last_pass<LOGN, 4, Mod32>(md, x, gtid, twg, inf.ninv, inf.wn);
+#pragma unroll
+      for (int pass = G_::NFULL - 1; pass >= 1; --pass) {
+        const int K = xpad_k(LOGN, 4, pass), S = xpad_s(LOGN, 4, pass);
+        if (pass == G_::NFULL - 1) {
+#pragma unroll
+          for (int e = 0; e < E; ++e) sm[xaddr_row<LOGN, 4>(gtid, e, K, S) - r * LP] = x[e];
+        } else {
+          group_sync<9>(tid, LOGN - (pass + 2) * 4);
+#pragma unroll
+          for (int e = 0; e < E; ++e) sm[xaddr_full<LOGN, 4>(pass + 1, gtid, e, K, S) - r * LP] = x[e];
+        }
+        group_sync<9>(tid, LOGN - (pass + 1) * 4);
+#pragma unroll
+        for (int e = 0; e < E; ++e) x[e] = sm[xaddr_full<LOGN, 4>(pass, gtid, e, K, S) - r * LP];
+        if (pass == 1) cluster_arrive();  // own tile reads done before the peer writes into it
+        inv_full_pass<LOGN, 4, Mod32>(md, x, pass, gtid, tws, inf.ninv, inf.wn);
+      }
+      cluster_wait();
+      {
+        // pass-1 layout -> pass-0 layout across the cluster: element i goes to
+        // CTA (i mod NT) / 512 at local index (i mod 512) + (i / NT) * 512
+        constexpr int K = xpad_k(LOGN, 4, 0), S = xpad_s(LOGN, 4, 0);
+        constexpr int TSH1 = LOGN - 8;
+        const int G1 = gtid >> TSH1, L1 = gtid & ((1 << TSH1) - 1);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int i = (G1 << (LOGN - 4)) + L1 + (e << TSH1);
+          const int owner = (i & (NT - 1)) >> 9;
+          const int li = (i & 511) + ((i >> (LOGN - 4)) << 9);
+          const int a = li + K * (li >> S);
+          if (owner == r)
+            sm[a] = x[e];
+          else
+            dsmem_st32(peer + 4u * (uint32_t)a, x[e]);
+        }
+        cluster_sync_all();
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int li = tid + (e << 9);
+          x[e] = sm[li + K * (li >> S)];
+        }
+      }
+      inv_full_pass<LOGN, 4, Mod32>(md, x, 0, gtid, tws, inf.ninv, inf.wn);
+      uint32_t* dst = out + poly(q);
+#pragma unroll
+      for (int e = 0; e < E; ++e) dst[gtid + e * NT] = md.subp(x[e]);
+    }
+  }
+  if (FWD) cluster_wait();  // pairs with the last arrive
+}
+
+static int ntt32_cluster_mode() {
+  static int m = -1;
+  if (m < 0) {
+    const char* v = std::getenv("HEFV_NTT32_CL");
+    m = v ? std::atoi(v) : 0;
+  }
+  return m;
+}
+
 // ---- batched device-order path for 64-bit primes, 2^10 <= N <= 2^14 --------
 // Same persistent prime-major schedule as k_ntt32_b.  STAGE: the prime's
 // full-pass twiddles (16-byte Shoup pairs) are staged in shared memory next
@@ -291,6 +511,17 @@ static int launch_b32(bool fwd, const uint32_t* in, uint32_t* out, int64_t batch
   typedef Geo<LOGN, 4> G_;
   const size_t smem = (size_t)(1 << (LOGN - G_::RLAST)) * sizeof(uint2) +
                       (size_t)((spad_size(G_::N) + 3) & ~3) * 4 + (size_t)G_::N * 4 + 16;
+  if (LOGN == 14 && ntt32_cluster_mode()) {
+    const size_t smc = (size_t)4096 * 8 + (size_t)((8704 + 4) & ~3) * 4 + 8192 * 4 + 16;
+    auto kc = fwd ? k_ntt32_cl<true> : k_ntt32_cl<false>;
+    HEFV_CUDA(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc));
+    const int64_t P = batch * nprimes;
+    int64_t ncl = (int64_t)sm_count();  // two CTAs per SM -> one cluster per SM
+    if (ncl > P) ncl = P;
+    kc<<<(unsigned)(2 * ncl), 512, smc, st>>>(in, out, batch, nprimes, prime_base, tw, info);
+    HEFV_LAUNCH_CHECK("k_ntt32_cl");
+    return 0;
+  }
   auto kern = fwd ? k_ntt32_b<LOGN, true> : k_ntt32_b<LOGN, false>;
   HEFV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 1;
@@ -424,6 +655,8 @@ using namespace hefv;
 
 int hefv_ntt64_large(hefv_ctx* c, bool fwd, const uint64_t* in, uint64_t* out, int64_t batch,
                      int nprimes, int prime_base, int natural, cudaStream_t st, int bcast = 0);
+int hefv_ntt32_large(hefv_ctx* c, bool fwd, const uint32_t* in, uint32_t* out, int64_t batch,
+                     int nprimes, int prime_base, int natural, cudaStream_t st);
 
 extern "C" {
 
@@ -434,7 +667,8 @@ int hefv_ntt_fwd32(hefv_ctx* c, const uint32_t* in, uint32_t* out, int64_t batch
     return fail("ntt_fwd32: prime range outside the context");
   int r = dispatch<Mod32>(c->log_n, true, in, out, batch, nprimes, prime_base, natural, c->d_tw32,
                           c->d_info32, as_stream(stream));
-  if (r == -100) return fail("ntt_fwd32: N = 2^16 is not supported for 32-bit primes");
+  if (r == -100) return hefv_ntt32_large(c, true, in, out, batch, nprimes, prime_base, natural,
+                                         as_stream(stream));
   return r;
 }
 
@@ -445,7 +679,8 @@ int hefv_ntt_inv32(hefv_ctx* c, const uint32_t* in, uint32_t* out, int64_t batch
     return fail("ntt_inv32: prime range outside the context");
   int r = dispatch<Mod32>(c->log_n, false, in, out, batch, nprimes, prime_base, natural,
                           c->d_itw32, c->d_info32, as_stream(stream));
-  if (r == -100) return fail("ntt_inv32: N = 2^16 is not supported for 32-bit primes");
+  if (r == -100) return hefv_ntt32_large(c, false, in, out, batch, nprimes, prime_base, natural,
+                                         as_stream(stream));
   return r;
 }
 
@@ -601,63 +836,44 @@ __global__ void k_permute_bitrev64(const uint64_t* __restrict__ in, uint64_t* __
 // ---------------------------------------------------------------------------
 namespace hefv {
 
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile(
-      "barrier.cluster.arrive.release.aligned;\n"
-      "barrier.cluster.wait.acquire.aligned;" ::
-          : "memory");
-}
-__device__ __forceinline__ uint32_t dsmem_map(uint32_t local_addr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_addr), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void dsmem_st64(uint32_t addr, uint64_t v) {
-  asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
-}
-
-template <int LOGN>
+template <int LOGN, class M>
 struct Cl64 {
   static constexpr int CL = 1 << (LOGN - 14);  // CTAs per cluster
   static constexpr int LOCAL = 1 << 14;        // words per CTA tile
   // every exchange pads with ratio 1/16 (xpad_k / xpad_s), so a CTA's block
   // [r LOCAL, (r+1) LOCAL) starts at padded address r * LP
   static constexpr int LP = LOCAL + LOCAL / 16;
-  static constexpr size_t smem = (size_t)((spad_size(LOCAL) + 1) & ~1) * 8;
+  static constexpr size_t smem = (size_t)((spad_size(LOCAL) + 3) & ~3) * sizeof(typename M::T);
 };
 
-template <int LOGN>
+__device__ __forceinline__ void dsmem_st(uint32_t addr, uint64_t v) { dsmem_st64(addr, v); }
+__device__ __forceinline__ void dsmem_st(uint32_t addr, uint32_t v) { dsmem_st32(addr, v); }
+
+template <int LOGN, class M, class TIn>
 __global__ void __cluster_dims__(1 << (LOGN - 14), 1, 1) __launch_bounds__(1024, 1)
-    k_ntt64_cl_fwd(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, int nprimes,
-                   int prime_base, const ulonglong2* __restrict__ tw_all,
-                   const Prime64Info* __restrict__ info, int bcast) {
+    k_ntt_cl_fwd(const TIn* __restrict__ in, typename M::T* __restrict__ out, int nprimes,
+                 int prime_base, const typename M::Tw* __restrict__ tw_all,
+                 const typename InfoOf<M>::I* __restrict__ info, int bcast) {
   typedef Geo<LOGN, 4> G_;
-  typedef Cl64<LOGN> C_;
+  typedef Cl64<LOGN, M> C_;
+  typedef typename M::T T;
   constexpr int E = 16, NT = G_::NT, LP = C_::LP;
   extern __shared__ __align__(16) unsigned char smraw[];
-  uint64_t* sm = reinterpret_cast<uint64_t*>(smraw);
+  T* sm = reinterpret_cast<T*>(smraw);
   const int tid = threadIdx.x;
   const int r = (int)cluster_ctarank();
   const int gtid = r * 1024 + tid;
   const size_t poly = blockIdx.x / C_::CL;
   const int pi = prime_base + (int)(poly % nprimes);
-  const uint64_t p = info[pi].p;
-  const Mod64 md{p, 2 * p};
-  const ulonglong2* tw = tw_all + (size_t)pi * G_::N;
-  const uint64_t* src = in + (bcast ? poly / nprimes : poly) * G_::N;
-  uint64_t* dst = out + poly * G_::N;
-  uint64_t x[E];
+  const auto* ip = info + pi;
+  const M md = make_mod(*ip);
+  const typename M::Tw* tw = tw_all + (size_t)pi * G_::N;
+  const TIn* src = in + (bcast ? poly / nprimes : poly) * G_::N;
+  T* dst = out + poly * G_::N;
+  T x[E];
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const uint64_t v = src[gtid + e * NT];
-    x[e] = v >= p ? barrett64(v, p, info[pi].mu) : v;
-  }
-  fwd_full_pass<LOGN, 4, Mod64>(md, x, 0, gtid, tw);
+  for (int e = 0; e < E; ++e) x[e] = cl_in(src[gtid + e * NT], *ip);
+  fwd_full_pass<LOGN, 4, M>(md, x, 0, gtid, tw);
   cluster_sync_all();  // every CTA of the cluster is running (its tile may be written)
   {
     constexpr int K = xpad_k(LOGN, 4, 0), S = xpad_s(LOGN, 4, 0);
@@ -666,7 +882,7 @@ __global__ void __cluster_dims__(1 << (LOGN - 14), 1, 1) __launch_bounds__(1024,
     for (int e = 0; e < E; ++e) {
       const int owner = e / (E / C_::CL);  // element gtid + e NT lives in block `owner`
       const int a = xaddr_full<LOGN, 4>(0, gtid, e, K, S) - owner * LP;
-      dsmem_st64(dsmem_map(base + 8u * (uint32_t)a, (uint32_t)owner), x[e]);
+      dsmem_st(dsmem_map(base + (uint32_t)(sizeof(T) * a), (uint32_t)owner), x[e]);
     }
     cluster_sync_all();
 #pragma unroll
@@ -674,7 +890,7 @@ __global__ void __cluster_dims__(1 << (LOGN - 14), 1, 1) __launch_bounds__(1024,
   }
 #pragma unroll
   for (int pass = 1; pass < G_::NFULL; ++pass) {
-    fwd_full_pass<LOGN, 4, Mod64>(md, x, pass, gtid, tw);
+    fwd_full_pass<LOGN, 4, M>(md, x, pass, gtid, tw);
     group_sync<10>(tid, LOGN - (pass + 1) * 4);
     const int K = xpad_k(LOGN, 4, pass), S = xpad_s(LOGN, 4, pass);
 #pragma unroll
@@ -688,36 +904,36 @@ __global__ void __cluster_dims__(1 << (LOGN - 14), 1, 1) __launch_bounds__(1024,
       for (int e = 0; e < E; ++e) x[e] = sm[xaddr_row<LOGN, 4>(gtid, e, K, S) - r * LP];
     }
   }
-  fwd_last_pass<LOGN, 4, Mod64>(md, x, gtid, tw);
+  fwd_last_pass<LOGN, 4, M>(md, x, gtid, tw);
 #pragma unroll
   for (int e = 0; e < E; ++e) x[e] = md.canon4(x[e]);
-  store_row_vec<LOGN, 4, uint64_t>(dst, gtid, x);
+  store_row_vec<LOGN, 4, T>(dst, gtid, x);
 }
 
-template <int LOGN>
+template <int LOGN, class M>
 __global__ void __cluster_dims__(1 << (LOGN - 14), 1, 1) __launch_bounds__(1024, 1)
-    k_ntt64_cl_inv(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, int nprimes,
-                   int prime_base, const ulonglong2* __restrict__ itw_all,
-                   const Prime64Info* __restrict__ info, int /*bcast*/) {
+    k_ntt_cl_inv(const typename M::T* __restrict__ in, typename M::T* __restrict__ out,
+                 int nprimes, int prime_base, const typename M::Tw* __restrict__ itw_all,
+                 const typename InfoOf<M>::I* __restrict__ info, int /*bcast*/) {
   typedef Geo<LOGN, 4> G_;
-  typedef Cl64<LOGN> C_;
+  typedef Cl64<LOGN, M> C_;
+  typedef typename M::T T;
   constexpr int E = 16, NT = G_::NT, LP = C_::LP;
   extern __shared__ __align__(16) unsigned char smraw[];
-  uint64_t* sm = reinterpret_cast<uint64_t*>(smraw);
+  T* sm = reinterpret_cast<T*>(smraw);
   const int tid = threadIdx.x;
   const int r = (int)cluster_ctarank();
   const int gtid = r * 1024 + tid;
   const size_t poly = blockIdx.x / C_::CL;
   const int pi = prime_base + (int)(poly % nprimes);
-  const Prime64Info* ip = info + pi;
-  const uint64_t p = ip->p;
-  const Mod64 md{p, 2 * p};
-  const ulonglong2* itw = itw_all + (size_t)pi * G_::N;
-  const uint64_t* src = in + poly * G_::N;
-  uint64_t* dst = out + poly * G_::N;
-  uint64_t x[E];
-  load_row_vec<LOGN, 4, uint64_t>(src, gtid, x);
-  inv_last_pass<LOGN, 4, Mod64>(md, x, gtid, itw, ip->ninv, ip->wn);
+  const auto* ip = info + pi;
+  const M md = make_mod(*ip);
+  const typename M::Tw* itw = itw_all + (size_t)pi * G_::N;
+  const T* src = in + poly * G_::N;
+  T* dst = out + poly * G_::N;
+  T x[E];
+  load_row_vec<LOGN, 4, T>(src, gtid, x);
+  inv_last_pass<LOGN, 4, M>(md, x, gtid, itw, ip->ninv, ip->wn);
 #pragma unroll
   for (int pass = G_::NFULL - 1; pass >= 1; --pass) {
     const int K = xpad_k(LOGN, 4, pass), S = xpad_s(LOGN, 4, pass);
@@ -732,7 +948,7 @@ __global__ void __cluster_dims__(1 << (LOGN - 14), 1, 1) __launch_bounds__(1024,
     group_sync<10>(tid, LOGN - (pass + 1) * 4);
 #pragma unroll
     for (int e = 0; e < E; ++e) x[e] = sm[xaddr_full<LOGN, 4>(pass, gtid, e, K, S) - r * LP];
-    inv_full_pass<LOGN, 4, Mod64>(md, x, pass, gtid, itw, ip->ninv, ip->wn);
+    inv_full_pass<LOGN, 4, M>(md, x, pass, gtid, itw, ip->ninv, ip->wn);
   }
   // exchange 0 (pass-1 layout -> pass-0 layout) through DSMEM: element i goes
   // to the CTA whose threads read it in pass 0, r' = (i mod NT) / 1024, at the
@@ -748,7 +964,8 @@ __global__ void __cluster_dims__(1 << (LOGN - 14), 1, 1) __launch_bounds__(1024,
       const int i = (G1 << (LOGN - 4)) + L1 + (e << TSH1);
       const int owner = (i & (NT - 1)) >> 10;
       const int li = (i & 1023) + ((i >> (LOGN - 4)) << 10);
-      dsmem_st64(dsmem_map(base + 8u * (uint32_t)(li + K * (li >> S)), (uint32_t)owner), x[e]);
+      dsmem_st(dsmem_map(base + (uint32_t)(sizeof(T) * (li + K * (li >> S))), (uint32_t)owner),
+               x[e]);
     }
     cluster_sync_all();
 #pragma unroll
@@ -757,23 +974,42 @@ __global__ void __cluster_dims__(1 << (LOGN - 14), 1, 1) __launch_bounds__(1024,
       x[e] = sm[li + K * (li >> S)];
     }
   }
-  inv_full_pass<LOGN, 4, Mod64>(md, x, 0, gtid, itw, ip->ninv, ip->wn);
+  inv_full_pass<LOGN, 4, M>(md, x, 0, gtid, itw, ip->ninv, ip->wn);
 #pragma unroll
   for (int e = 0; e < E; ++e) dst[gtid + e * NT] = md.subp(x[e]);
+}
+
+template <int LOGN, class M, class TIn>
+static int launch_cl(bool fwd, const TIn* in, typename M::T* out, int64_t total_polys,
+                     int nprimes, int prime_base, const typename M::Tw* tw,
+                     const typename InfoOf<M>::I* info, cudaStream_t st, int bcast) {
+  typedef Cl64<LOGN, M> C_;
+  if (total_polys * C_::CL > 0x7fffffff) return fail("ntt: batch too large");
+  if (fwd) {
+    auto kern = k_ntt_cl_fwd<LOGN, M, TIn>;
+    HEFV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C_::smem));
+    kern<<<(unsigned)(total_polys * C_::CL), 1024, C_::smem, st>>>(in, out, nprimes, prime_base, tw,
+                                                                   info, bcast);
+  } else {
+    if constexpr (sizeof(TIn) == sizeof(typename M::T)) {
+      auto kern = k_ntt_cl_inv<LOGN, M>;
+      HEFV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C_::smem));
+      kern<<<(unsigned)(total_polys * C_::CL), 1024, C_::smem, st>>>(
+          reinterpret_cast<const typename M::T*>(in), out, nprimes, prime_base, tw, info, bcast);
+    } else {
+      return fail("ntt: inverse input must have the word type");
+    }
+  }
+  HEFV_LAUNCH_CHECK("k_ntt_cl");
+  return 0;
 }
 
 template <int LOGN>
 static int launch_cl64(bool fwd, const uint64_t* in, uint64_t* out, int64_t total_polys,
                        int nprimes, int prime_base, const ulonglong2* tw,
                        const Prime64Info* info, cudaStream_t st, int bcast) {
-  typedef Cl64<LOGN> C_;
-  auto kern = fwd ? k_ntt64_cl_fwd<LOGN> : k_ntt64_cl_inv<LOGN>;
-  HEFV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C_::smem));
-  if (total_polys * C_::CL > 0x7fffffff) return fail("ntt64: batch too large");
-  kern<<<(unsigned)(total_polys * C_::CL), 1024, C_::smem, st>>>(in, out, nprimes, prime_base, tw,
-                                                                 info, bcast);
-  HEFV_LAUNCH_CHECK("k_ntt64_cl");
-  return 0;
+  return launch_cl<LOGN, Mod64, uint64_t>(fwd, in, out, total_polys, nprimes, prime_base, tw, info,
+                                          st, bcast);
 }
 
 static bool ntt64_cluster_enabled() {
@@ -892,4 +1128,50 @@ int hefv_ntt64_large(hefv_ctx* c, bool fwd, const uint64_t* in, uint64_t* out, i
   }
   (void)blocks16;
   return 0;
+}
+
+// 32-bit primes at N = 2^16: the cluster transform (device order only).
+int hefv_ntt32_large(hefv_ctx* c, bool fwd, const uint32_t* in, uint32_t* out, int64_t batch,
+                     int nprimes, int prime_base, int natural, cudaStream_t st) {
+  if (c->log_n != 16) return fail("ntt32: unsupported ring dimension");
+  if (natural) return fail("ntt32: N = 2^16 runs in device order only");
+  return launch_cl<16, Mod32, uint32_t>(fwd, in, out, batch * nprimes, nprimes, prime_base,
+                                        fwd ? c->d_tw32 : c->d_itw32, c->d_info32, st, 0);
+}
+
+// Forward transforms (device order) of u64 rows (< 2^62) under the 32-bit
+// primes [prime_base, prime_base + nprimes): out[r][t] = NTT_t(in[r] mod a_t).
+// Internal: the aux-basis 64-bit key switch feeds its digits through this.
+int hefv_ntt32_fwd_rows64(hefv_ctx* c, const uint64_t* in, uint32_t* out, int64_t rows,
+                          int nprimes, int prime_base, cudaStream_t st) {
+  const int64_t total = rows * nprimes;
+  if (total <= 0) return 0;
+  if (total > 0x7fffffff) return fail("ntt32_rows64: batch too large");
+  switch (c->log_n) {
+#define HEFV_R64(L)                                                                          \
+  case L: {                                                                                  \
+    typedef Geo<L, 4> G_;                                                                    \
+    const size_t smem = (size_t)spad_size(G_::N) * 4;                                        \
+    auto kern = k_ntt_fwd<L, 4, Mod32, uint64_t>;                                            \
+    HEFV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    kern<<<(unsigned)total, G_::NT, smem, st>>>(in, out, nprimes, prime_base, 0, c->d_tw32,  \
+                                                c->d_info32, 1);                             \
+    HEFV_LAUNCH_CHECK("k_ntt_fwd rows64");                                                   \
+    return 0;                                                                                \
+  }
+    HEFV_R64(10)
+    HEFV_R64(11)
+    HEFV_R64(12)
+    HEFV_R64(13)
+    HEFV_R64(14)
+#undef HEFV_R64
+    case 15:
+      return launch_cl<15, Mod32, uint64_t>(true, in, out, total, nprimes, prime_base, c->d_tw32,
+                                            c->d_info32, st, 1);
+    case 16:
+      return launch_cl<16, Mod32, uint64_t>(true, in, out, total, nprimes, prime_base, c->d_tw32,
+                                            c->d_info32, st, 1);
+    default:
+      return fail("ntt32_rows64: ring dimension outside 2^10..2^16");
+  }
 }

@@ -310,6 +310,48 @@ def test_ntt64_device_order_matches_oracle(log_n, bits):
     lib.hefv_ctx_destroy(h)
 
 
+@pytest.mark.parametrize("log_n", [10, 12, 13, 14])
+def test_ntt32_device_order_matches_oracle(log_n):
+    """Batched 30-bit device-order transforms (the persistent k_ntt32_b /
+    cluster path, prime boundaries inside CTA ranges, inputs up to 2^32 - 1)
+    equal the oracle's natural-order NTT permuted into bit-reversed order,
+    and invert to x mod p."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1901_10074_b200 import _native as nat
+    from paper_1901_10074_b200.ring import root_of_unity
+
+    n = 1 << log_n
+    L, B = 3, 7
+    primes = O.ntt_primes(L, 30, 2 * n)
+    psis = [root_of_unity(p, n) for p in primes]
+    lib = nat.load()
+    h = C.c_void_p()
+    nat.check(lib.hefv_ctx_create(C.byref(h), log_n, L, (C.c_uint32 * L)(*primes),
+                                  (C.c_uint32 * L)(*psis), 0, None, None))
+    g = np.random.default_rng(log_n)
+    xs = g.integers(0, 1 << 32, (B, L, n), dtype=np.uint64).astype(np.uint32)
+    x = torch.from_numpy(xs.view(np.int32)).cuda()
+    y = torch.empty_like(x)
+    z = torch.empty_like(x)
+    st = torch.cuda.current_stream().cuda_stream
+    nat.check(lib.hefv_ntt_fwd32(h, x.data_ptr(), y.data_ptr(), B, L, 0, 0, st))
+    nat.check(lib.hefv_ntt_inv32(h, y.data_ptr(), z.data_ptr(), B, L, 0, 0, st))
+    got = y.cpu().numpy().view(np.uint32)
+    back = z.cpu().numpy().view(np.uint32)
+    rev = np.array([int(format(i, f"0{log_n}b")[::-1], 2) for i in range(n)])
+    for j, p in enumerate(primes):
+        ref = O.OracleNtt(p, n)
+        for b in (0, 3, B - 1):
+            red = xs[b, j].astype(np.int64) % p
+            want = np.asarray(ref.fwd(red), dtype=np.int64)[rev]
+            assert np.array_equal(got[b, j].astype(np.int64), want), (b, j)
+            assert np.array_equal(back[b, j].astype(np.int64), red), (b, j)
+    lib.hefv_ctx_destroy(h)
+
+
 @pytest.mark.parametrize("name", ["desk", "retina"])
 def test_mul_plain_and_keyswitch_batch_stress(name):
     import torch

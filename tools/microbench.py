@@ -70,7 +70,8 @@ def ks_case(log_n, bits, L, B):
     t = timeit(lambda: ks.switch(key, dig), iters=3)
     modmuls = (L * L + 2 * L) * ((n // 2) * log_n + n) + 2 * L * L * n
     return {"cts_s": round(B / t, 1), "us_per_ct": round(t / B * 1e6, 2),
-            "Tmodmul_s": round(modmuls * B / t / 1e12, 4)}
+            "Tmodmul_s": round(modmuls * B / t / 1e12, 4),
+            "path": "aux" if ks.aux else "direct"}
 
 
 def main():
