@@ -203,3 +203,24 @@ def test_simulator_config1_matches_plaintext_mod_t():
     assert [int(v) for v in logits] == g["logits"]
     assert [int(v) for v in logits] == centred_mod(plaintext_forward(net, img),
                                                    params.plain_modulus)
+
+
+def test_ks64_aux_prime_count_covers_the_exactness_bound():
+    """rns.aux_prime_count: the aux basis of the 64-bit key switch must exceed
+    8 L N max(p)^2 (ks64_aux.cu) for every config-4 shape; the setup rejects
+    a basis that does not (checked on the GPU side as well)."""
+    import math
+
+    from paper_1901_10074_b200.ring import find_ntt_primes
+    from paper_1901_10074_b200.rns import aux_prime_count
+
+    for log_n in (10, 12, 14, 16):
+        for L in (1, 2, 4, 8):
+            for bits in (50, 60, 62):
+                primes = find_ntt_primes(L, bits, 2 << log_n)
+                T = aux_prime_count(primes, log_n)
+                aux = find_ntt_primes(T, 30, 2 << log_n, below=int(2 ** 29.5))
+                need = 3 + math.log2(L) + log_n + 2 * math.log2(max(primes))
+                assert sum(math.log2(a) for a in aux) > need + 0.01
+                assert max(aux) ** 2 * L < 2 ** 62  # MAC sums stay below 2^62
+                assert T <= 6
