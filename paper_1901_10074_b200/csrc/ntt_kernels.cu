@@ -195,213 +195,6 @@ __global__ void __launch_bounds__(Geo<LOGN, 4>::NT, 1024 / Geo<LOGN, 4>::NT)
   }
 }
 
-// ---- 30-bit, N = 2^14: one 2-CTA cluster per polynomial ---------------------
-// Experimental (HEFV_NTT32_CL=1).  The 16384-word transform of k_ntt32_b over
-// a cluster of two 512-thread CTAs (16 words per thread, 8192-word tile
-// each), so two independent transforms share every SM (two CTAs of different
-// clusters) and one CTA's barrier / exchange phase overlaps the other's
-// butterflies.  The exchange whose group spans the whole polynomial (forward:
-// exchange 0; inverse: its last) writes into the owning CTA's tile through
-// DSMEM.  Persistent: cluster c owns the polynomial range [c P / G, (c+1) P /
-// G) in prime-major order; every input half is bulk-copied one transform
-// ahead.
-template <bool FWD>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 2)
-    k_ntt32_cl(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int64_t batch,
-               int nprimes, int prime_base, const uint2* __restrict__ tw_all,
-               const Prime32Info* __restrict__ info) {
-  constexpr int LOGN = 14;
-  typedef Geo<LOGN, 4> G_;  // over the cluster: NT = 1024 global threads
-  constexpr int E = 16, NT = G_::NT, N = G_::N, HALF = N / 2;
-  constexpr int NTW = 1 << (LOGN - G_::RLAST);
-  constexpr int LP = HALF + HALF / 16;  // padded words per CTA block (ratio 1/16)
-  extern __shared__ __align__(16) unsigned char smraw[];
-  uint2* tws = reinterpret_cast<uint2*>(smraw);
-  uint32_t* sm = reinterpret_cast<uint32_t*>(tws + NTW);
-  uint32_t* stage = sm + ((LP + 4) & ~3);
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(stage + HALF);
-  const int tid = threadIdx.x;
-  const int r = (int)cluster_ctarank();
-  const int gtid = r * 512 + tid;
-  const int64_t ncl = gridDim.x >> 1, cid = blockIdx.x >> 1;
-  const int64_t P = batch * nprimes;
-  const int64_t qbeg = P * cid / ncl, qend = P * (cid + 1) / ncl;
-  auto poly = [&](int64_t q) {
-    const int64_t j = q / batch, b = q - j * batch;
-    return (b * nprimes + j) * (int64_t)N;
-  };
-  // this CTA's input: forward = column layout elements e*1024 + 512r + [0,512)
-  // (16 runs of 2 KB), inverse = row layout block [r HALF, (r+1) HALF)
-  auto issue = [&](int64_t q) {
-    const uint32_t* src = in + poly(q);
-    const uint32_t m = (uint32_t)__cvta_generic_to_shared(mbar);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(m), "r"(HALF * 4)
-                 : "memory");
-    if constexpr (FWD) {
-#pragma unroll 1
-      for (int e = 0; e < E; ++e) {
-        const uint32_t d = (uint32_t)__cvta_generic_to_shared(stage + e * 512);
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-            ::"r"(d), "l"(src + e * 1024 + 512 * r), "r"(2048), "r"(m) : "memory");
-      }
-    } else {
-      const uint32_t d = (uint32_t)__cvta_generic_to_shared(stage);
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-          ::"r"(d), "l"(src + r * HALF), "r"(HALF * 4), "r"(m) : "memory");
-    }
-  };
-  if (tid == 0) {
-    mbar_init(mbar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (qbeg < qend && tid == 0) issue(qbeg);
-  cluster_arrive();  // pairs with the first pre-exchange wait (peer started)
-  uint32_t phase = 0;
-  int cur = -1;
-  Prime32Info inf;
-  const uint2* twg = nullptr;
-  const uint32_t base = (uint32_t)__cvta_generic_to_shared(sm);
-  const uint32_t peer = dsmem_map(base, (uint32_t)(r ^ 1));
-  for (int64_t q = qbeg; q < qend; ++q) {
-    const int j = (int)(q / batch);
-    if (j != cur) {
-      cur = j;
-      inf = info[prime_base + j];
-      twg = tw_all + (size_t)(prime_base + j) * N;
-      __syncthreads();
-      const uint4* src = reinterpret_cast<const uint4*>(twg);
-      uint4* dst = reinterpret_cast<uint4*>(tws);
-      for (int i = tid; i < NTW / 2; i += 512) dst[i] = __ldg(src + i);
-      __syncthreads();
-    }
-    const Mod32 md{inf.p, 2 * inf.p};
-    mbar_wait(mbar, phase);
-    phase ^= 1u;
-    uint32_t x[E];
-    const bool more = q + 1 < qend;
-    if constexpr (FWD) {
-      if (inf.p > (1u << 29) && inf.p < (1u << 30)) {
-        const uint32_t p4 = 4 * inf.p;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const uint32_t v = stage[e * 512 + tid];
-          x[e] = min(v, v - p4);
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const uint32_t v = stage[e * 512 + tid];
-          x[e] = inf.p >= (1u << 30) ? v : barrett62(v, inf.p, inf.mu);
-        }
-      }
-      fwd_full_pass<LOGN, 4, Mod32>(md, x, 0, gtid, tws);
-      cluster_wait();  // the peer is done reading its tile (previous transform)
-      {
-        constexpr int K = xpad_k(LOGN, 4, 0), S = xpad_s(LOGN, 4, 0);
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int owner = e >> 3;  // element gtid + e NT lives in block e / 8
-          const int a = xaddr_full<LOGN, 4>(0, gtid, e, K, S) - owner * LP;
-          if (owner == r)
-            sm[a] = x[e];
-          else
-            dsmem_st32(peer + 4u * (uint32_t)a, x[e]);
-        }
-        cluster_sync_all();
-        if (tid == 0 && more) issue(q + 1);  // every local thread has read its stage words
-#pragma unroll
-        for (int e = 0; e < E; ++e) x[e] = sm[xaddr_full<LOGN, 4>(1, gtid, e, K, S) - r * LP];
-      }
-#pragma unroll
-      for (int pass = 1; pass < G_::NFULL; ++pass) {
-        fwd_full_pass<LOGN, 4, Mod32>(md, x, pass, gtid, tws);
-        group_sync<9>(tid, LOGN - (pass + 1) * 4);
-        const int K = xpad_k(LOGN, 4, pass), S = xpad_s(LOGN, 4, pass);
-#pragma unroll
-        for (int e = 0; e < E; ++e) sm[xaddr_full<LOGN, 4>(pass, gtid, e, K, S) - r * LP] = x[e];
-        group_sync<9>(tid, LOGN - (pass + 1) * 4);
-        if (pass + 1 < G_::NFULL) {
-#pragma unroll
-          for (int e = 0; e < E; ++e) x[e] = sm[xaddr_full<LOGN, 4>(pass + 1, gtid, e, K, S) - r * LP];
-        } else {
-#pragma unroll
-          for (int e = 0; e < E; ++e) x[e] = sm[xaddr_row<LOGN, 4>(gtid, e, K, S) - r * LP];
-        }
-      }
-      cluster_arrive();  // this CTA's tile reads of this transform are done
-      fwd_last_pass<LOGN, 4, Mod32>(md, x, gtid, twg);
-#pragma unroll
-      for (int e = 0; e < E; ++e) x[e] = md.canon4(x[e]);
-      store_row_vec<LOGN, 4, uint32_t>(out + poly(q), gtid, x);
-    } else {
-      load_row16_smem(stage, tid, x);
-      __syncthreads();  // stage consumed; the previous transform's tile reads are done
-      if (tid == 0 && more) issue(q + 1);
-      inv_last_pass<LOGN, 4, Mod32>(md, x, gtid, twg, inf.ninv, inf.wn);
-#pragma unroll
-      for (int pass = G_::NFULL - 1; pass >= 1; --pass) {
-        const int K = xpad_k(LOGN, 4, pass), S = xpad_s(LOGN, 4, pass);
-        if (pass == G_::NFULL - 1) {
-#pragma unroll
-          for (int e = 0; e < E; ++e) sm[xaddr_row<LOGN, 4>(gtid, e, K, S) - r * LP] = x[e];
-        } else {
-          group_sync<9>(tid, LOGN - (pass + 2) * 4);
-#pragma unroll
-          for (int e = 0; e < E; ++e) sm[xaddr_full<LOGN, 4>(pass + 1, gtid, e, K, S) - r * LP] = x[e];
-        }
-        group_sync<9>(tid, LOGN - (pass + 1) * 4);
-#pragma unroll
-        for (int e = 0; e < E; ++e) x[e] = sm[xaddr_full<LOGN, 4>(pass, gtid, e, K, S) - r * LP];
-        if (pass == 1) cluster_arrive();  // own tile reads done before the peer writes into it
-        inv_full_pass<LOGN, 4, Mod32>(md, x, pass, gtid, tws, inf.ninv, inf.wn);
-      }
-      cluster_wait();
-      {
-        // pass-1 layout -> pass-0 layout across the cluster: element i goes to
-        // CTA (i mod NT) / 512 at local index (i mod 512) + (i / NT) * 512
-        constexpr int K = xpad_k(LOGN, 4, 0), S = xpad_s(LOGN, 4, 0);
-        constexpr int TSH1 = LOGN - 8;
-        const int G1 = gtid >> TSH1, L1 = gtid & ((1 << TSH1) - 1);
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int i = (G1 << (LOGN - 4)) + L1 + (e << TSH1);
-          const int owner = (i & (NT - 1)) >> 9;
-          const int li = (i & 511) + ((i >> (LOGN - 4)) << 9);
-          const int a = li + K * (li >> S);
-          if (owner == r)
-            sm[a] = x[e];
-          else
-            dsmem_st32(peer + 4u * (uint32_t)a, x[e]);
-        }
-        cluster_sync_all();
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int li = tid + (e << 9);
-          x[e] = sm[li + K * (li >> S)];
-        }
-      }
-      inv_full_pass<LOGN, 4, Mod32>(md, x, 0, gtid, tws, inf.ninv, inf.wn);
-      uint32_t* dst = out + poly(q);
-#pragma unroll
-      for (int e = 0; e < E; ++e) dst[gtid + e * NT] = md.subp(x[e]);
-    }
-  }
-  if (FWD) cluster_wait();  // pairs with the last arrive
-}
-
-static int ntt32_cluster_mode() {
-  static int m = -1;
-  if (m < 0) {
-    const char* v = std::getenv("HEFV_NTT32_CL");
-    m = v ? std::atoi(v) : 0;
-  }
-  return m;
-}
-
 // ---- batched device-order path for 64-bit primes, 2^10 <= N <= 2^14 --------
 // Same persistent prime-major schedule as k_ntt32_b.  STAGE: the prime's
 // full-pass twiddles (16-byte Shoup pairs) are staged in shared memory next
@@ -511,17 +304,6 @@ static int launch_b32(bool fwd, const uint32_t* in, uint32_t* out, int64_t batch
   typedef Geo<LOGN, 4> G_;
   const size_t smem = (size_t)(1 << (LOGN - G_::RLAST)) * sizeof(uint2) +
                       (size_t)((spad_size(G_::N) + 3) & ~3) * 4 + (size_t)G_::N * 4 + 16;
-  if (LOGN == 14 && ntt32_cluster_mode()) {
-    const size_t smc = (size_t)4096 * 8 + (size_t)((8704 + 4) & ~3) * 4 + 8192 * 4 + 16;
-    auto kc = fwd ? k_ntt32_cl<true> : k_ntt32_cl<false>;
-    HEFV_CUDA(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc));
-    const int64_t P = batch * nprimes;
-    int64_t ncl = (int64_t)sm_count();  // two CTAs per SM -> one cluster per SM
-    if (ncl > P) ncl = P;
-    kc<<<(unsigned)(2 * ncl), 512, smc, st>>>(in, out, batch, nprimes, prime_base, tw, info);
-    HEFV_LAUNCH_CHECK("k_ntt32_cl");
-    return 0;
-  }
   auto kern = fwd ? k_ntt32_b<LOGN, true> : k_ntt32_b<LOGN, false>;
   HEFV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 1;
