@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
 #endif
 constexpr int KSA_STAGES = KSA_STAGES_V;  // depth of the digit-tile ring
 
+
 __device__ __forceinline__ void mad_wide(uint64_t& acc, uint32_t a, uint32_t b) {
   asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc) : "r"(a), "r"(b));
 }
@@ -305,8 +306,11 @@ __global__ void __launch_bounds__(32 * (JW + 2), 1)
     for (int it = 0; it < 5; ++it) inv *= 2u - red.a * inv;
     red.nainv = 0u - inv;
   }
-  // packed key pairs (k_2u : k_2u+1) of body and mask, and their pair sums
-  uint64_t kb[H], km[H];
+  // Two ciphertexts per iteration (twice the independent multiply chains per
+  // warp): the mask key pairs move to (dynamic) shared memory, [u][warp][lane],
+  // to free the registers; the body key pairs stay in registers.
+  extern __shared__ __align__(16) uint64_t kms[];
+  uint64_t kb[H];
   uint64_t kpb = 0, kpm = 0;
   {
     const size_t kstride = (size_t)k * k * n;  // body -> mask rows of the same t
@@ -319,36 +323,53 @@ __global__ void __launch_bounds__(32 * (JW + 2), 1)
       const uint32_t m0 = i0 < k ? __ldg(ks + kstride + 32 * i0) : 0u;
       const uint32_t m1 = i1 < k ? __ldg(ks + kstride + 32 * i1) : 0u;
       kb[u] = ((uint64_t)b0 << 32) | b1;
-      km[u] = ((uint64_t)m0 << 32) | m1;
+      kms[(u * JW + w) * 32 + lane] = ((uint64_t)m0 << 32) | m1;
       mad_wide(kpb, b0, b1);
       mad_wide(kpm, m0, m1);
     }
   }
+  const uint64_t* kmw = kms + w * 32 + lane;
   uint32_t* yb = Y + (((size_t)bbeg * 3 + t) * 2 * k + j) * (size_t)n + (m << 5) + lane;
   const size_t ymask = (size_t)k * n;
   const size_t ystride = (size_t)3 * 2 * k * n;
-  for (int r = 0; r < nb; ++r) {
-    const int st = r % S;
-    mbw(xready0 + 8 * st, (uint32_t)((r / S) & 1));
-    const uint2* xs = &xx[st][0][lane];
-    uint64_t b0 = 0, b1 = 0, m0 = 0, m1 = 0;
+  for (int r = 0; r < nb; r += 2) {
+    const int st0 = r % S, st1 = (r + 1) % S;
+    const bool two = r + 1 < nb;
+    mbw(xready0 + 8 * st0, (uint32_t)((r / S) & 1));
+    if (two) mbw(xready0 + 8 * st1, (uint32_t)(((r + 1) / S) & 1));
+    const uint2* xs0 = &xx[st0][0][lane];
+    const uint2* xs1 = &xx[st1][0][lane];
+    uint64_t b0 = 0, m0 = 0, b1 = 0, m1 = 0;
 #pragma unroll
     for (int u = 0; u < H; ++u) {
-      // (x_2u+1 : x_2u) + (k_2u : k_2u+1) = (x_2u+1 + k_2u : x_2u + k_2u+1)
-      const uint2 xv = xs[32 * u];
-      const uint64_t xw = ((uint64_t)xv.y << 32) | xv.x;
-      const uint64_t sb = xw + kb[u], sm = xw + km[u];
-      mad_wide((u & 1) ? b1 : b0, (uint32_t)sb, (uint32_t)(sb >> 32));
-      mad_wide((u & 1) ? m1 : m0, (uint32_t)sm, (uint32_t)(sm >> 32));
+      const uint2 xv0 = xs0[32 * u];
+      const uint2 xv1 = two ? xs1[32 * u] : make_uint2(0u, 0u);
+      const uint64_t kmu = kmw[u * JW * 32];
+      const uint64_t xw0 = ((uint64_t)xv0.y << 32) | xv0.x;
+      const uint64_t xw1 = ((uint64_t)xv1.y << 32) | xv1.x;
+      const uint64_t sb0 = xw0 + kb[u], sm0 = xw0 + kmu;
+      const uint64_t sb1 = xw1 + kb[u], sm1 = xw1 + kmu;
+      mad_wide(b0, (uint32_t)sb0, (uint32_t)(sb0 >> 32));
+      mad_wide(m0, (uint32_t)sm0, (uint32_t)(sm0 >> 32));
+      mad_wide(b1, (uint32_t)sb1, (uint32_t)(sb1 >> 32));
+      mad_wide(m1, (uint32_t)sm1, (uint32_t)(sm1 >> 32));
     }
-    const uint64_t xp = xpair[st][lane];
+    const uint64_t xp0 = xpair[st0][lane];
+    const uint64_t xp1 = two ? xpair[st1][lane] : 0ull;
     __syncwarp();
-    if (lane == 0) mba(xempty0 + 8 * st);
-    if (active) {
-      yb[0] = red(b0 + b1 - xp - kpb);
-      yb[ymask] = red(m0 + m1 - xp - kpm);
+    if (lane == 0) {
+      mba(xempty0 + 8 * st0);
+      if (two) mba(xempty0 + 8 * st1);
     }
-    yb += ystride;
+    if (active) {
+      yb[0] = red(b0 - xp0 - kpb);
+      yb[ymask] = red(m0 - xp0 - kpm);
+      if (two) {
+        yb[ystride] = red(b1 - xp1 - kpb);
+        yb[ystride + ymask] = red(m1 - xp1 - kpm);
+      }
+    }
+    yb += 2 * ystride;
   }
 }
 
@@ -586,14 +607,27 @@ static int run_ksa_e(hefv_ctx* c, const uint32_t* kaux, const uint32_t* dig, int
       dim3 grid((unsigned)(3 * (n >> 5)), (unsigned)((nb + KSA_MAC_CTS - 1) / KSA_MAC_CTS));
       // consumer warps per CTA: all k target primes where the key registers
       // fit (k <= 22), else the primes split over blockIdx.z
+      // the mask key pairs live in dynamic shared memory (H x JW x 32 words)
+      auto dyn = [](int K, int JW) { return (size_t)(K / 2) * JW * 32 * 8; };
       if (k == 22) {
-        k_ksa_mac<22, 22><<<grid, 32 * 24, 0, st>>>(X, kaux, Y, nb, k, c->log_n, ab, c->d_info32);
+        HEFV_CUDA(cudaFuncSetAttribute(k_ksa_mac<22, 22>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)dyn(22, 22)));
+        k_ksa_mac<22, 22><<<grid, 32 * 24, dyn(22, 22), st>>>(X, kaux, Y, nb, k, c->log_n, ab,
+                                                               c->d_info32);
       } else if (k <= 16) {
-        k_ksa_mac<16, 16><<<grid, 32 * 18, 0, st>>>(X, kaux, Y, nb, k, c->log_n, ab, c->d_info32);
+        HEFV_CUDA(cudaFuncSetAttribute(k_ksa_mac<16, 16>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)dyn(16, 16)));
+        k_ksa_mac<16, 16><<<grid, 32 * 18, dyn(16, 16), st>>>(X, kaux, Y, nb, k, c->log_n, ab,
+                                                               c->d_info32);
       } else {
         dim3 g2(grid.x, grid.y, (unsigned)((k + 11) / 12));
-        k_ksa_mac<KSA_KMAX, 12><<<g2, 32 * 14, 0, st>>>(X, kaux, Y, nb, k, c->log_n, ab,
-                                                         c->d_info32);
+        HEFV_CUDA(cudaFuncSetAttribute(k_ksa_mac<KSA_KMAX, 12>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)dyn(KSA_KMAX, 12)));
+        k_ksa_mac<KSA_KMAX, 12><<<g2, 32 * 14, dyn(KSA_KMAX, 12), st>>>(X, kaux, Y, nb, k,
+                                                                        c->log_n, ab, c->d_info32);
       }
       HEFV_LAUNCH_CHECK("k_ksa_mac");
     }
