@@ -380,8 +380,8 @@ def _ntt_microbench(peaks=None):
 
     lib = nat.load()
     res, fracs = {}, {}
-    for log_n, bits, L, batch in [(16, 60, 8, 64), (14, 60, 8, 256), (12, 50, 8, 1024),
-                                  (14, 30, 22, 256)]:
+    for log_n, bits, L, batch in [(16, 60, 8, 64), (15, 55, 8, 128), (14, 60, 8, 256),
+                                  (13, 60, 8, 256), (12, 50, 8, 1024), (14, 30, 22, 256)]:
         n = 1 << log_n
         primes = find_ntt_primes(L, bits, 2 * n)
         psis = [root_of_unity(p, n) for p in primes]
@@ -423,6 +423,43 @@ def _ntt_microbench(peaks=None):
     out = {"unit": "limb-polys/s", **res}
     if peaks:
         out["roofline"] = fracs
+    out["keyswitch64"] = _ks64_microbench(peaks)
+    return out
+
+
+def _ks64_microbench(peaks=None):
+    """Config 4: a full key switch over L = 8 60-bit primes (the reference's
+    _keyswitch_apply, fv.py:205-217), ciphertexts/s; roofline in the
+    reference formulation's (L^2 + 2L)((N/2) log2 N + N) + 2 L^2 N modmuls per
+    ciphertext against the measured 64-bit butterfly rate."""
+    import torch
+
+    from paper_1901_10074_b200.ring import find_ntt_primes
+    from paper_1901_10074_b200.rns import RnsKeySwitch64
+
+    out = {"unit": "us per ciphertext"}
+    for log_n, L, B in [(14, 8, 32), (16, 8, 8)]:
+        n = 1 << log_n
+        ks = RnsKeySwitch64(find_ntt_primes(L, 60, 2 * n), n)
+        key = ks.random_key(1)
+        p = torch.tensor(ks.primes, dtype=torch.int64, device="cuda").view(1, L, 1)
+        dig = torch.randint(0, 1 << 62, (B, L, n), dtype=torch.int64, device="cuda") % p
+        ks.switch(key, dig)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(3):
+            ks.switch(key, dig)
+        b.record()
+        torch.cuda.synchronize()
+        us = a.elapsed_time(b) / 3 / B * 1e3
+        mm = (L * L + 2 * L) * ((n // 2) * log_n + n) + 2 * L * L * n
+        ent = {"us_per_ct": round(us, 2), "path": "aux" if ks.aux else "direct",
+               "ref_Tmodmul_s": round(mm / us / 1e6, 3)}
+        if peaks:
+            ent["frac_of_64bit_butterfly_peak"] = round(mm / us / 1e6 / peaks["shoup_butterfly64"], 3)
+        out[f"N=2^{log_n},60-bit,L={L},B={B}"] = ent
+        del ks
     return out
 
 
