@@ -82,21 +82,35 @@ __device__ __forceinline__ void cp_async_wait() {
 // (cp.async.bulk) into a staging buffer one transform ahead, the copy issued
 // right after the current transform's first CTA barrier.
 template <int LOGN, int LOGE>
+struct KsaFwdSmem {
+  typedef Geo<LOGN, LOGE> G_;
+  static constexpr bool LASTSM = LOGN == 14 && LOGE == 4;
+  static constexpr int NTW = 1 << (LOGN - G_::RLAST);
+  static constexpr size_t bytes = (size_t)NTW * sizeof(uint2) +
+                                  (size_t)((spad_size(G_::N) + 3) & ~3) * 4 + (size_t)G_::N * 4 +
+                                  16 + (LASTSM ? (size_t)(G_::N - NTW) * 4 : 0);
+};
+
+template <int LOGN, int LOGE>
 __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
     k_ksa_fwd(const uint32_t* __restrict__ digits, int64_t dig_stride,
               const int32_t* __restrict__ dslot, uint32_t ginv, uint32_t* __restrict__ X,
               int64_t B, int k, int aux_base, const uint2* __restrict__ tw_all,
-              const Prime32Info* __restrict__ info) {
+              const Prime32Info* __restrict__ info, const uint32_t* __restrict__ twm_all) {
   typedef Geo<LOGN, LOGE> G_;
   constexpr int E = G_::E;
   constexpr int NT = G_::NT;
   constexpr int N = G_::N;
   constexpr int NTW = 1 << (LOGN - G_::RLAST);
+  // the last pass's twiddles as single-word Montgomery forms in shared memory
+  // (see k_ntt32_b): 48 KB at 2^14, instead of L2-latency-bound Shoup loads
+  constexpr bool LASTSM = KsaFwdSmem<LOGN, LOGE>::LASTSM;
   extern __shared__ __align__(16) unsigned char smraw[];
   uint2* tws = reinterpret_cast<uint2*>(smraw);
   uint32_t* sm = reinterpret_cast<uint32_t*>(tws + NTW);
   uint32_t* stage = sm + ((spad_size(N) + 3) & ~3);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(stage + N);
+  uint32_t* twl = reinterpret_cast<uint32_t*>(mbar + 2);
   const int t = blockIdx.x / k;
   const int i = blockIdx.x - t * k;
   const int tid = threadIdx.x;
@@ -113,6 +127,11 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
     const uint4* src = reinterpret_cast<const uint4*>(twg);
     uint4* dst = reinterpret_cast<uint4*>(tws);
     for (int q = tid; q < NTW / 2; q += NT) dst[q] = __ldg(src + q);
+    if constexpr (LASTSM) {
+      const uint4* srcm = reinterpret_cast<const uint4*>(twm_all + (size_t)(aux_base + t) * N + NTW);
+      uint4* dstm = reinterpret_cast<uint4*>(twl);
+      for (int q = tid; q < (N - NTW) / 4; q += NT) dstm[q] = __ldg(srcm + q);
+    }
   }
   __syncthreads();
   // digit row i of ciphertext b (through the slot map when given)
@@ -144,7 +163,13 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
     auto hook = [&]() {
       if (tid == 0 && nxt) bulk_g2s(stage, nxt, N * 4, mbar);
     };
-    cta_fwd<LOGN, LOGE, Mod32>(md, x, sm, tws, twg, hook, LOGN - G_::RLAST);
+    if constexpr (LASTSM) {
+      cta_fwd<LOGN, LOGE, Mod32, decltype(hook), false>(md, x, sm, tws, twg, hook);
+      const Mod32M mm{inf.p, 2 * inf.p, inf.pinv};
+      fwd_last_pass<LOGN, LOGE, Mod32M>(mm, x, tid, twl - NTW);
+    } else {
+      cta_fwd<LOGN, LOGE, Mod32>(md, x, sm, tws, twg, hook, LOGN - G_::RLAST);
+    }
 #pragma unroll
     for (int e = 0; e < E; ++e) x[e] = md.canon4(x[e]);
     store_tiled<LOGN, LOGE>(X + ((size_t)b * 3 + t) * k * (size_t)N, k, i, tid, x);
@@ -587,8 +612,7 @@ static int run_ksa_e(hefv_ctx* c, const uint32_t* kaux, const uint32_t* dig, int
   auto kf = k_ksa_fwd<LOGN, LF>;
   auto ki = k_ksa_inv<LOGN, LI>;
   const size_t tile = (size_t)((spad_size(GF::N) + 3) & ~3) * 4;
-  const size_t smf = (size_t)(1 << (LOGN - GF::RLAST)) * sizeof(uint2) + tile +
-                     (size_t)GF::N * 4 + 16;
+  const size_t smf = KsaFwdSmem<LOGN, LF>::bytes;
   const size_t smi = tile + (size_t)GI::N * 2 + (size_t)GI::N * 4 + 16;
   HEFV_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smf));
   HEFV_CUDA(cudaFuncSetAttribute(ki, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smi));
@@ -600,7 +624,7 @@ static int run_ksa_e(hefv_ctx* c, const uint32_t* kaux, const uint32_t* dig, int
     {
       dim3 grid((unsigned)(3 * k), (unsigned)((nb + KSA_FWD_CTS - 1) / KSA_FWD_CTS));
       kf<<<grid, GF::NT, smf, st>>>(dslot ? dig : dig + c0 * ds, ds, dslot ? dslot + c0 : nullptr,
-                                    ginv, X, nb, k, ab, c->d_tw32, c->d_info32);
+                                    ginv, X, nb, k, ab, c->d_tw32, c->d_info32, c->d_twm32);
       HEFV_LAUNCH_CHECK("k_ksa_fwd");
     }
     {

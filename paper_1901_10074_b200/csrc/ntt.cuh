@@ -60,7 +60,19 @@ __device__ __forceinline__ int row_index(int tid, int e) {
 // twiddles with 16-byte accesses where possible.
 template <class Tw, int MAXC>
 __device__ __forceinline__ void load_tw_run(const Tw* __restrict__ p, Tw* out, const int count) {
-  if (sizeof(Tw) == 8 && count % 2 == 0) {
+  if (sizeof(Tw) == 4 && count % 4 == 0) {  // single-word (Montgomery) twiddles
+    const uint4* q = reinterpret_cast<const uint4*>(p);
+#pragma unroll
+    for (int i = 0; i < MAXC / 4; ++i) {
+      if (4 * i < count) {
+        const uint4 v = q[i];
+        out[4 * i] = *reinterpret_cast<const Tw*>(&v.x);
+        out[4 * i + 1] = *reinterpret_cast<const Tw*>(&v.y);
+        out[4 * i + 2] = *reinterpret_cast<const Tw*>(&v.z);
+        out[4 * i + 3] = *reinterpret_cast<const Tw*>(&v.w);
+      }
+    }
+  } else if (sizeof(Tw) == 8 && count % 2 == 0) {
     const uint4* q = reinterpret_cast<const uint4*>(p);
 #pragma unroll
     for (int i = 0; i < MAXC / 2; ++i) {
@@ -255,7 +267,7 @@ struct NoHook {
 // `hook` runs right after the first CTA-wide barrier of the transform, i.e.
 // once every thread has consumed its input registers' source (used to
 // recycle an input staging buffer).
-template <int LOGN, int LOGE, class M, class Hook = NoHook>
+template <int LOGN, int LOGE, class M, class Hook = NoHook, bool LAST = true>
 __device__ __forceinline__ void cta_fwd(const M& md, typename M::T* x, typename M::T* sm,
                                         const typename M::Tw* __restrict__ tw,
                                         const typename M::Tw* __restrict__ tw_last = nullptr,
@@ -287,6 +299,8 @@ __device__ __forceinline__ void cta_fwd(const M& md, typename M::T* x, typename 
     }
   }
   // last pass: stages with table entries below 2^split_log from `tw`, the rest from tw_last
+  // (LAST = false: the caller runs it, e.g. with another twiddle form)
+  if (!LAST) return;
   if (tw_last == nullptr)
     fwd_last_pass<LOGN, LOGE, M>(md, x, tid, tw);
   else

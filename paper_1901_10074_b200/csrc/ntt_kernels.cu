@@ -109,21 +109,37 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT)
 // bulk-copied (cp.async.bulk) into a staging buffer one transform ahead (the
 // copy is issued right after the current transform's first CTA barrier).
 
+// LASTSM (forward): the last pass's twiddles (entries [NTW, N), 48 KB at
+// 2^14) also live in shared memory, as single-word Montgomery forms (the
+// Shoup pairs would not fit next to the tile and the stage); the last pass
+// then uses Montgomery products instead of L2-latency-bound Shoup loads.
+template <int LOGN, bool FWD>
+struct Ntt32B {
+  typedef Geo<LOGN, 4> G_;
+  static constexpr bool LASTSM = FWD && LOGN == 14;
+  static constexpr int NTW = 1 << (LOGN - G_::RLAST);
+  static constexpr size_t smem = (size_t)NTW * sizeof(uint2) +
+                                 (size_t)((spad_size(G_::N) + 3) & ~3) * 4 + (size_t)G_::N * 4 +
+                                 16 + (LASTSM ? (size_t)(G_::N - NTW) * 4 : 0);
+};
+
 template <int LOGN, bool FWD>
 __global__ void __launch_bounds__(Geo<LOGN, 4>::NT, 1024 / Geo<LOGN, 4>::NT)
     k_ntt32_b(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int64_t batch,
               int nprimes, int prime_base, const uint2* __restrict__ tw_all,
-              const Prime32Info* __restrict__ info) {
+              const Prime32Info* __restrict__ info, const uint32_t* __restrict__ twm_all) {
   typedef Geo<LOGN, 4> G_;
   constexpr int E = G_::E;
   constexpr int NT = G_::NT;
   constexpr int N = G_::N;
   constexpr int NTW = 1 << (LOGN - G_::RLAST);
+  constexpr bool LASTSM = Ntt32B<LOGN, FWD>::LASTSM;
   extern __shared__ __align__(16) unsigned char smraw[];
   uint2* tws = reinterpret_cast<uint2*>(smraw);
   uint32_t* sm = reinterpret_cast<uint32_t*>(tws + NTW);
   uint32_t* stage = sm + ((spad_size(N) + 3) & ~3);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(stage + N);
+  uint32_t* twl = reinterpret_cast<uint32_t*>(mbar + 2);  // LASTSM: entries [NTW, N)
   const int tid = threadIdx.x;
   const int64_t P = batch * nprimes;
   const int64_t qbeg = P * blockIdx.x / gridDim.x;
@@ -154,6 +170,11 @@ __global__ void __launch_bounds__(Geo<LOGN, 4>::NT, 1024 / Geo<LOGN, 4>::NT)
       const uint4* src = reinterpret_cast<const uint4*>(twg);
       uint4* dst = reinterpret_cast<uint4*>(tws);
       for (int i = tid; i < NTW / 2; i += NT) dst[i] = __ldg(src + i);
+      if constexpr (LASTSM) {
+        const uint4* srcm = reinterpret_cast<const uint4*>(twm_all + (size_t)(prime_base + j) * N + NTW);
+        uint4* dstm = reinterpret_cast<uint4*>(twl);
+        for (int i = tid; i < (N - NTW) / 4; i += NT) dstm[i] = __ldg(srcm + i);
+      }
       __syncthreads();
     }
     const Mod32 md{inf.p, 2 * inf.p};
@@ -181,7 +202,13 @@ __global__ void __launch_bounds__(Geo<LOGN, 4>::NT, 1024 / Geo<LOGN, 4>::NT)
 #pragma unroll
         for (int e = 0; e < E; ++e) x[e] = barrett62(stage[tid + e * NT], inf.p, inf.mu);
       }
-      cta_fwd<LOGN, 4, Mod32>(md, x, sm, tws, twg, hook, LOGN - G_::RLAST);
+      if constexpr (LASTSM) {
+        cta_fwd<LOGN, 4, Mod32, decltype(hook), false>(md, x, sm, tws, twg, hook);
+        const Mod32M mm{inf.p, 2 * inf.p, inf.pinv};
+        fwd_last_pass<LOGN, 4, Mod32M>(mm, x, tid, twl - NTW);
+      } else {
+        cta_fwd<LOGN, 4, Mod32>(md, x, sm, tws, twg, hook, LOGN - G_::RLAST);
+      }
 #pragma unroll
       for (int e = 0; e < E; ++e) x[e] = md.canon4(x[e]);
       store_row_vec<LOGN, 4, uint32_t>(out + poly(q), tid, x);
@@ -300,10 +327,10 @@ static int sm_count() {
 
 template <int LOGN>
 static int launch_b32(bool fwd, const uint32_t* in, uint32_t* out, int64_t batch, int nprimes,
-                      int prime_base, const uint2* tw, const Prime32Info* info, cudaStream_t st) {
+                      int prime_base, const uint2* tw, const Prime32Info* info, cudaStream_t st,
+                      const uint32_t* twm) {
   typedef Geo<LOGN, 4> G_;
-  const size_t smem = (size_t)(1 << (LOGN - G_::RLAST)) * sizeof(uint2) +
-                      (size_t)((spad_size(G_::N) + 3) & ~3) * 4 + (size_t)G_::N * 4 + 16;
+  const size_t smem = fwd ? Ntt32B<LOGN, true>::smem : Ntt32B<LOGN, false>::smem;
   auto kern = fwd ? k_ntt32_b<LOGN, true> : k_ntt32_b<LOGN, false>;
   HEFV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 1;
@@ -313,7 +340,7 @@ static int launch_b32(bool fwd, const uint32_t* in, uint32_t* out, int64_t batch
   const int64_t P = batch * nprimes;
   const int64_t slots = (int64_t)sm_count() * per_sm;
   const unsigned grid = (unsigned)(P < slots ? P : slots);
-  kern<<<grid, G_::NT, smem, st>>>(in, out, batch, nprimes, prime_base, tw, info);
+  kern<<<grid, G_::NT, smem, st>>>(in, out, batch, nprimes, prime_base, tw, info, twm);
   HEFV_LAUNCH_CHECK("k_ntt32_b");
   return 0;
 }
@@ -358,7 +385,8 @@ static int launch_b64(bool fwd, const uint64_t* in, uint64_t* out, int64_t batch
 template <int LOGN, int LOGE, class M>
 static int launch_one(bool fwd, const typename M::T* in, typename M::T* out, int64_t batch,
                       int nprimes, int prime_base, int natural, const typename M::Tw* tw,
-                      const typename InfoOf<M>::I* info, cudaStream_t st, int bcast) {
+                      const typename InfoOf<M>::I* info, cudaStream_t st, int bcast,
+                      const uint32_t* twm) {
   typedef Geo<LOGN, LOGE> G_;
   const size_t smem = (size_t)spad_size(G_::N) * sizeof(typename M::T);
   const int64_t total = batch * nprimes;
@@ -369,7 +397,7 @@ static int launch_one(bool fwd, const typename M::T* in, typename M::T* out, int
       return launch_b32<LOGN>(fwd, reinterpret_cast<const uint32_t*>(in),
                               reinterpret_cast<uint32_t*>(out), batch, nprimes, prime_base,
                               reinterpret_cast<const uint2*>(tw),
-                              reinterpret_cast<const Prime32Info*>(info), st);
+                              reinterpret_cast<const Prime32Info*>(info), st, twm);
   }
   if constexpr (sizeof(typename M::T) == 8 && LOGN >= 10 && LOGN <= 14 && LOGE == 4) {
     const int mode = ntt64_mode(LOGN, fwd);
@@ -398,17 +426,17 @@ template <class M>
 static int dispatch(int log_n, bool fwd, const typename M::T* in, typename M::T* out,
                     int64_t batch, int nprimes, int prime_base, int natural,
                     const typename M::Tw* tw, const typename InfoOf<M>::I* info, cudaStream_t st,
-                    int bcast = 0) {
+                    int bcast = 0, const uint32_t* twm = nullptr) {
 #define HEFV_CASE(L) \
   case L:            \
-    return launch_one<L, 4, M>(fwd, in, out, batch, nprimes, prime_base, natural, tw, info, st, bcast);
+    return launch_one<L, 4, M>(fwd, in, out, batch, nprimes, prime_base, natural, tw, info, st, bcast, twm);
   switch (log_n) {
     case 1:
-      return launch_one<1, 1, M>(fwd, in, out, batch, nprimes, prime_base, natural, tw, info, st, bcast);
+      return launch_one<1, 1, M>(fwd, in, out, batch, nprimes, prime_base, natural, tw, info, st, bcast, twm);
     case 2:
-      return launch_one<2, 2, M>(fwd, in, out, batch, nprimes, prime_base, natural, tw, info, st, bcast);
+      return launch_one<2, 2, M>(fwd, in, out, batch, nprimes, prime_base, natural, tw, info, st, bcast, twm);
     case 3:
-      return launch_one<3, 3, M>(fwd, in, out, batch, nprimes, prime_base, natural, tw, info, st, bcast);
+      return launch_one<3, 3, M>(fwd, in, out, batch, nprimes, prime_base, natural, tw, info, st, bcast, twm);
     HEFV_CASE(4)
     HEFV_CASE(5)
     HEFV_CASE(6)
@@ -426,7 +454,7 @@ static int dispatch(int log_n, bool fwd, const typename M::T* in, typename M::T*
 #undef HEFV_CASE
   if constexpr (sizeof(typename M::T) == 4) {
     if (log_n == 15)
-      return launch_one<15, 5, M>(fwd, in, out, batch, nprimes, prime_base, natural, tw, info, st, bcast);
+      return launch_one<15, 5, M>(fwd, in, out, batch, nprimes, prime_base, natural, tw, info, st, bcast, twm);
   }
   return -100;  // not handled by the CTA-resident path
 }
@@ -448,7 +476,7 @@ int hefv_ntt_fwd32(hefv_ctx* c, const uint32_t* in, uint32_t* out, int64_t batch
   if (nprimes < 1 || prime_base < 0 || prime_base + nprimes > c->n32)
     return fail("ntt_fwd32: prime range outside the context");
   int r = dispatch<Mod32>(c->log_n, true, in, out, batch, nprimes, prime_base, natural, c->d_tw32,
-                          c->d_info32, as_stream(stream));
+                          c->d_info32, as_stream(stream), 0, c->d_twm32);
   if (r == -100) return hefv_ntt32_large(c, true, in, out, batch, nprimes, prime_base, natural,
                                          as_stream(stream));
   return r;
