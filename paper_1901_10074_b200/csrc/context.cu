@@ -113,7 +113,7 @@ int hefv_ctx_create(hefv_ctx** out, uint32_t log_n, int32_t n32, const uint32_t*
   // ---- 32-bit primes
   c->n32 = n32;
   std::vector<uint2> tw((size_t)n32 * n), itw((size_t)n32 * n);
-  std::vector<uint32_t> twm((size_t)n32 * n);
+  std::vector<uint32_t> twm((size_t)n32 * n), itwm((size_t)n32 * n);
   for (int i = 0; i < n32; ++i) {
     const uint64_t p = primes32[i];
     if (p >= (1ull << 30) || p < 3) {
@@ -131,6 +131,7 @@ int hefv_ctx_create(hefv_ctx** out, uint32_t log_n, int32_t n32, const uint32_t*
       tw[(size_t)i * n + j] = make_uint2((uint32_t)f[j], (uint32_t)((f[j] << 32) / p));
       itw[(size_t)i * n + j] = make_uint2((uint32_t)v[j], (uint32_t)((v[j] << 32) / p));
       twm[(size_t)i * n + j] = (uint32_t)((f[j] << 32) % p);
+      itwm[(size_t)i * n + j] = (uint32_t)((v[j] << 32) % p);
     }
     Prime32Info inf{};
     inf.p = (uint32_t)p;
@@ -200,6 +201,7 @@ int hefv_ctx_create(hefv_ctx** out, uint32_t log_n, int32_t n32, const uint32_t*
   up((void**)&c->d_itw32, itw.data(), itw.size() * sizeof(uint2));
   up((void**)&c->d_info32, c->info32.data(), c->info32.size() * sizeof(Prime32Info));
   up((void**)&c->d_twm32, twm.data(), twm.size() * sizeof(uint32_t));
+  up((void**)&c->d_itwm32, itwm.data(), itwm.size() * sizeof(uint32_t));
   up((void**)&c->d_tw64, tw64.data(), tw64.size() * sizeof(ulonglong2));
   up((void**)&c->d_itw64, itw64.data(), itw64.size() * sizeof(ulonglong2));
   up((void**)&c->d_info64, c->info64.data(), c->info64.size() * sizeof(Prime64Info));
@@ -217,6 +219,7 @@ void hefv_ctx_destroy(hefv_ctx* c) {
   cudaFree(c->d_itw32);
   cudaFree(c->d_info32);
   cudaFree(c->d_twm32);
+  cudaFree(c->d_itwm32);
   cudaFree(c->d_tw64);
   cudaFree(c->d_itw64);
   cudaFree(c->d_info64);

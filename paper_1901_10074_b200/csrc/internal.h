@@ -29,7 +29,8 @@ struct hefv_ctx {
   std::vector<uint32_t> primes32;
   uint2* d_tw32 = nullptr;    // (n32, N) forward twiddles (psi^bitrev, shoup)
   uint2* d_itw32 = nullptr;   // (n32, N) inverse twiddles
-  uint32_t* d_twm32 = nullptr;  // (n32, N) forward twiddles, Montgomery form
+  uint32_t* d_twm32 = nullptr;   // (n32, N) forward twiddles, Montgomery form
+  uint32_t* d_itwm32 = nullptr;  // (n32, N) inverse twiddles, Montgomery form
   hefv::Prime32Info* d_info32 = nullptr;
   std::vector<hefv::Prime32Info> info32;
   // 64-bit prime set: plaintext modulus t (FV) or microbench primes

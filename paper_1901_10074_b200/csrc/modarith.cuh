@@ -78,6 +78,18 @@ struct Mod32M {
     x = a + t;
     y = a - t + p2;
   }
+  // Gentleman-Sande, inputs < 2p -> outputs < 2p (as Mod32::gs)
+  __device__ __forceinline__ void gs(uint32_t& x, uint32_t& y, Tw w) const {
+    uint32_t a = x, b = y;
+    x = sub2p(a + b);
+    y = mul(a - b + p2, w);
+  }
+  // last inverse stage with N^{-1} merged (Montgomery-form ninv, wn)
+  __device__ __forceinline__ void gs_last(uint32_t& x, uint32_t& y, Tw ninv, Tw wn) const {
+    uint32_t a = x, b = y;
+    x = mul(a + b, ninv);
+    y = mul(a - b + p2, wn);
+  }
 };
 
 // Montgomery REDC for a*b with b < p and a < 2^32: returns a*b*2^-32 mod p in [0, 2p).

@@ -404,7 +404,9 @@ __device__ __forceinline__ void inv_full_pass(const M& md, typename M::T* x, int
 // full-pass entries staged in shared memory as `itw`, the rest from global).
 // `hook` runs right after the transform's first CTA-wide barrier (every
 // thread has consumed its input registers' source by then).
-template <int LOGN, int LOGE, class M, class Hook = NoHook>
+// FIRST = false: the caller has run the first (register-only) pass itself,
+// e.g. with another twiddle form.
+template <int LOGN, int LOGE, class M, class Hook = NoHook, bool FIRST = true>
 __device__ __forceinline__ void cta_inv(const M& md, typename M::T* x, typename M::T* sm,
                                         const typename M::Tw* __restrict__ itw,
                                         const typename M::Tw& ninv, const typename M::Tw& wn,
@@ -413,7 +415,7 @@ __device__ __forceinline__ void cta_inv(const M& md, typename M::T* x, typename 
   typedef Geo<LOGN, LOGE> G_;
   constexpr int LOG_NT = LOGN - LOGE;
   const int tid = threadIdx.x;
-  inv_last_pass<LOGN, LOGE, M>(md, x, tid, itw_last ? itw_last : itw, ninv, wn);
+  if (FIRST) inv_last_pass<LOGN, LOGE, M>(md, x, tid, itw_last ? itw_last : itw, ninv, wn);
 #pragma unroll
   for (int pass = G_::NFULL - 1; pass >= 0; --pass) {
     // group of this exchange: threads sharing a pass-`pass` region

@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT)
 template <int LOGN, bool FWD>
 struct Ntt32B {
   typedef Geo<LOGN, 4> G_;
-  static constexpr bool LASTSM = FWD && LOGN == 14;
+  static constexpr bool LASTSM = LOGN == 14;  // fwd: last pass; inv: its first pass
   static constexpr int NTW = 1 << (LOGN - G_::RLAST);
   static constexpr size_t smem = (size_t)NTW * sizeof(uint2) +
                                  (size_t)((spad_size(G_::N) + 3) & ~3) * 4 + (size_t)G_::N * 4 +
@@ -214,7 +214,13 @@ __global__ void __launch_bounds__(Geo<LOGN, 4>::NT, 1024 / Geo<LOGN, 4>::NT)
       store_row_vec<LOGN, 4, uint32_t>(out + poly(q), tid, x);
     } else {
       load_row16_smem(stage, tid, x);
-      cta_inv<LOGN, 4, Mod32>(md, x, sm, tws, inf.ninv, inf.wn, twg, hook);
+      if constexpr (LASTSM) {
+        const Mod32M mm{inf.p, 2 * inf.p, inf.pinv};
+        inv_last_pass<LOGN, 4, Mod32M>(mm, x, tid, twl - NTW, 0u, 0u);  // N^-1 is in pass 0
+        cta_inv<LOGN, 4, Mod32, decltype(hook), false>(md, x, sm, tws, inf.ninv, inf.wn, twg, hook);
+      } else {
+        cta_inv<LOGN, 4, Mod32>(md, x, sm, tws, inf.ninv, inf.wn, twg, hook);
+      }
       uint32_t* dst = out + poly(q);
 #pragma unroll
       for (int e = 0; e < E; ++e) dst[tid + e * NT] = md.subp(x[e]);
@@ -488,7 +494,7 @@ int hefv_ntt_inv32(hefv_ctx* c, const uint32_t* in, uint32_t* out, int64_t batch
   if (nprimes < 1 || prime_base < 0 || prime_base + nprimes > c->n32)
     return fail("ntt_inv32: prime range outside the context");
   int r = dispatch<Mod32>(c->log_n, false, in, out, batch, nprimes, prime_base, natural,
-                          c->d_itw32, c->d_info32, as_stream(stream));
+                          c->d_itw32, c->d_info32, as_stream(stream), 0, c->d_itwm32);
   if (r == -100) return hefv_ntt32_large(c, false, in, out, batch, nprimes, prime_base, natural,
                                          as_stream(stream));
   return r;
