@@ -331,6 +331,7 @@ __global__ void __launch_bounds__(32 * (JW + 2), 1)
     for (int it = 0; it < 5; ++it) inv *= 2u - red.a * inv;
     red.nainv = 0u - inv;
   }
+  if constexpr (JW == 22) {
   // Two ciphertexts per iteration (twice the independent multiply chains per
   // warp): the mask key pairs move to (dynamic) shared memory, [u][warp][lane],
   // to free the registers; the body key pairs stay in registers.
@@ -395,6 +396,53 @@ __global__ void __launch_bounds__(32 * (JW + 2), 1)
       }
     }
     yb += 2 * ystride;
+  }
+  } else {
+  // packed key pairs (k_2u : k_2u+1) of body and mask, and their pair sums
+  uint64_t kb[H], km[H];
+  uint64_t kpb = 0, kpm = 0;
+  {
+    const size_t kstride = (size_t)k * k * n;  // body -> mask rows of the same t
+    const uint32_t* ks = kaux + (((size_t)t * 2 * k + j) * tiles + m) * k * 32 + lane;
+#pragma unroll
+    for (int u = 0; u < H; ++u) {
+      const int i0 = 2 * u, i1 = 2 * u + 1;
+      const uint32_t b0 = i0 < k ? __ldg(ks + 32 * i0) : 0u;
+      const uint32_t b1 = i1 < k ? __ldg(ks + 32 * i1) : 0u;
+      const uint32_t m0 = i0 < k ? __ldg(ks + kstride + 32 * i0) : 0u;
+      const uint32_t m1 = i1 < k ? __ldg(ks + kstride + 32 * i1) : 0u;
+      kb[u] = ((uint64_t)b0 << 32) | b1;
+      km[u] = ((uint64_t)m0 << 32) | m1;
+      mad_wide(kpb, b0, b1);
+      mad_wide(kpm, m0, m1);
+    }
+  }
+  uint32_t* yb = Y + (((size_t)bbeg * 3 + t) * 2 * k + j) * (size_t)n + (m << 5) + lane;
+  const size_t ymask = (size_t)k * n;
+  const size_t ystride = (size_t)3 * 2 * k * n;
+  for (int r = 0; r < nb; ++r) {
+    const int st = r % S;
+    mbw(xready0 + 8 * st, (uint32_t)((r / S) & 1));
+    const uint2* xs = &xx[st][0][lane];
+    uint64_t b0 = 0, b1 = 0, m0 = 0, m1 = 0;
+#pragma unroll
+    for (int u = 0; u < H; ++u) {
+      // (x_2u+1 : x_2u) + (k_2u : k_2u+1) = (x_2u+1 + k_2u : x_2u + k_2u+1)
+      const uint2 xv = xs[32 * u];
+      const uint64_t xw = ((uint64_t)xv.y << 32) | xv.x;
+      const uint64_t sb = xw + kb[u], sm = xw + km[u];
+      mad_wide((u & 1) ? b1 : b0, (uint32_t)sb, (uint32_t)(sb >> 32));
+      mad_wide((u & 1) ? m1 : m0, (uint32_t)sm, (uint32_t)(sm >> 32));
+    }
+    const uint64_t xp = xpair[st][lane];
+    __syncwarp();
+    if (lane == 0) mba(xempty0 + 8 * st);
+    if (active) {
+      yb[0] = red(b0 + b1 - xp - kpb);
+      yb[ymask] = red(m0 + m1 - xp - kpm);
+    }
+    yb += ystride;
+  }
   }
 }
 
@@ -632,7 +680,7 @@ static int run_ksa_e(hefv_ctx* c, const uint32_t* kaux, const uint32_t* dig, int
       // consumer warps per CTA: all k target primes where the key registers
       // fit (k <= 22), else the primes split over blockIdx.z
       // the mask key pairs live in dynamic shared memory (H x JW x 32 words)
-      auto dyn = [](int K, int JW) { return (size_t)(K / 2) * JW * 32 * 8; };
+      auto dyn = [](int K, int JW) { return JW == 22 ? (size_t)(K / 2) * JW * 32 * 8 : (size_t)0; };
       if (k == 22) {
         HEFV_CUDA(cudaFuncSetAttribute(k_ksa_mac<22, 22>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -18,7 +18,12 @@ from paper_1901_10074_b200.ring import galois_element
 name = sys.argv[1] if len(sys.argv) > 1 else "retina"
 B = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
 iters = int(sys.argv[3]) if len(sys.argv) > 3 else 3
-p = profile(name)
+if name.startswith("config"):
+    from paper_1901_10074_b200.configs import config_params
+
+    p = config_params(int(name[6:]))
+else:
+    p = profile(name)
 be = FvBackend(p, rng=np.random.default_rng(1))
 ctx = be.ctx
 assert ctx.ks_aux, "profile does not use the aux-basis key switch"
