@@ -106,6 +106,7 @@ int hefv_ctx_create(hefv_ctx** out, uint32_t log_n, int32_t n32, const uint32_t*
   if (const char* v = std::getenv("HEFV_KS_TMEM")) c->ks_tmem = std::atoi(v);
   if (const char* v = std::getenv("HEFV_KS_E32")) c->ks_e32 = std::atoi(v);
   if (const char* v = std::getenv("HEFV_KS_PREFETCH")) c->ks_prefetch = std::atoi(v);
+  if (const char* v = std::getenv("HEFV_KSA_MAC24")) c->ksa_mac24 = std::atoi(v);
   c->log_n = (int)log_n;
   c->n = 1 << log_n;
   const int n = c->n;

@@ -184,6 +184,9 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
 #define KSA_STAGES_V 4
 #endif
 constexpr int KSA_STAGES = KSA_STAGES_V;  // depth of the digit-tile ring
+#ifndef KSA_MAC_ALLSMEM
+#define KSA_MAC_ALLSMEM 0  // k = 22 MAC: body key pairs in shared memory too (A/B)
+#endif
 
 
 __device__ __forceinline__ void mad_wide(uint64_t& acc, uint32_t a, uint32_t b) {
@@ -331,12 +334,15 @@ __global__ void __launch_bounds__(32 * (JW + 2), 1)
     for (int it = 0; it < 5; ++it) inv *= 2u - red.a * inv;
     red.nainv = 0u - inv;
   }
-  if constexpr (JW == 22) {
+  if constexpr (JW >= 22) {
   // Two ciphertexts per iteration (twice the independent multiply chains per
   // warp): the mask key pairs move to (dynamic) shared memory, [u][warp][lane],
-  // to free the registers; the body key pairs stay in registers.
+  // to free the registers; the body key pairs stay in registers unless ALLS
+  // (all key pairs in shared memory, [u][part][warp][lane]: the 24-warp CTA of
+  // k = 23, 24, whose register budget is 78 per thread).
+  constexpr bool ALLS = JW > 22 || KSA_MAC_ALLSMEM;
   extern __shared__ __align__(16) uint64_t kms[];
-  uint64_t kb[H];
+  uint64_t kb[ALLS ? 1 : H];
   uint64_t kpb = 0, kpm = 0;
   {
     const size_t kstride = (size_t)k * k * n;  // body -> mask rows of the same t
@@ -348,8 +354,13 @@ __global__ void __launch_bounds__(32 * (JW + 2), 1)
       const uint32_t b1 = i1 < k ? __ldg(ks + 32 * i1) : 0u;
       const uint32_t m0 = i0 < k ? __ldg(ks + kstride + 32 * i0) : 0u;
       const uint32_t m1 = i1 < k ? __ldg(ks + kstride + 32 * i1) : 0u;
-      kb[u] = ((uint64_t)b0 << 32) | b1;
-      kms[(u * JW + w) * 32 + lane] = ((uint64_t)m0 << 32) | m1;
+      if constexpr (ALLS) {
+        kms[((2 * u) * JW + w) * 32 + lane] = ((uint64_t)b0 << 32) | b1;
+        kms[((2 * u + 1) * JW + w) * 32 + lane] = ((uint64_t)m0 << 32) | m1;
+      } else {
+        kb[u] = ((uint64_t)b0 << 32) | b1;
+        kms[(u * JW + w) * 32 + lane] = ((uint64_t)m0 << 32) | m1;
+      }
       mad_wide(kpb, b0, b1);
       mad_wide(kpm, m0, m1);
     }
@@ -370,11 +381,18 @@ __global__ void __launch_bounds__(32 * (JW + 2), 1)
     for (int u = 0; u < H; ++u) {
       const uint2 xv0 = xs0[32 * u];
       const uint2 xv1 = two ? xs1[32 * u] : make_uint2(0u, 0u);
-      const uint64_t kmu = kmw[u * JW * 32];
+      uint64_t kbu, kmu;
+      if constexpr (ALLS) {
+        kbu = kmw[(2 * u) * JW * 32];
+        kmu = kmw[(2 * u + 1) * JW * 32];
+      } else {
+        kbu = kb[u];
+        kmu = kmw[u * JW * 32];
+      }
       const uint64_t xw0 = ((uint64_t)xv0.y << 32) | xv0.x;
       const uint64_t xw1 = ((uint64_t)xv1.y << 32) | xv1.x;
-      const uint64_t sb0 = xw0 + kb[u], sm0 = xw0 + kmu;
-      const uint64_t sb1 = xw1 + kb[u], sm1 = xw1 + kmu;
+      const uint64_t sb0 = xw0 + kbu, sm0 = xw0 + kmu;
+      const uint64_t sb1 = xw1 + kbu, sm1 = xw1 + kmu;
       mad_wide(b0, (uint32_t)sb0, (uint32_t)(sb0 >> 32));
       mad_wide(m0, (uint32_t)sm0, (uint32_t)(sm0 >> 32));
       mad_wide(b1, (uint32_t)sb1, (uint32_t)(sb1 >> 32));
@@ -679,8 +697,13 @@ static int run_ksa_e(hefv_ctx* c, const uint32_t* kaux, const uint32_t* dig, int
       dim3 grid((unsigned)(3 * (n >> 5)), (unsigned)((nb + KSA_MAC_CTS - 1) / KSA_MAC_CTS));
       // consumer warps per CTA: all k target primes where the key registers
       // fit (k <= 22), else the primes split over blockIdx.z
-      // the mask key pairs live in dynamic shared memory (H x JW x 32 words)
-      auto dyn = [](int K, int JW) { return JW == 22 ? (size_t)(K / 2) * JW * 32 * 8 : (size_t)0; };
+      // the 22- and 24-warp CTAs keep key pairs in dynamic shared memory:
+      // mask pairs (H x JW x 32 words), or body and mask pairs (ALLS)
+      auto dyn = [](int K, int JW) -> size_t {
+        if (JW < 22) return 0;
+        const bool alls = JW > 22 || KSA_MAC_ALLSMEM;
+        return (size_t)(K / 2) * JW * 32 * 8 * (alls ? 2 : 1);
+      };
       if (k == 22) {
         HEFV_CUDA(cudaFuncSetAttribute(k_ksa_mac<22, 22>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -688,18 +711,17 @@ static int run_ksa_e(hefv_ctx* c, const uint32_t* kaux, const uint32_t* dig, int
         k_ksa_mac<22, 22><<<grid, 32 * 24, dyn(22, 22), st>>>(X, kaux, Y, nb, k, c->log_n, ab,
                                                                c->d_info32);
       } else if (k <= 16) {
-        HEFV_CUDA(cudaFuncSetAttribute(k_ksa_mac<16, 16>,
+        k_ksa_mac<16, 16><<<grid, 32 * 18, 0, st>>>(X, kaux, Y, nb, k, c->log_n, ab, c->d_info32);
+      } else if (k > 22 && c->ksa_mac24) {
+        HEFV_CUDA(cudaFuncSetAttribute(k_ksa_mac<24, 24>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)dyn(16, 16)));
-        k_ksa_mac<16, 16><<<grid, 32 * 18, dyn(16, 16), st>>>(X, kaux, Y, nb, k, c->log_n, ab,
+                                       (int)dyn(24, 24)));
+        k_ksa_mac<24, 24><<<grid, 32 * 26, dyn(24, 24), st>>>(X, kaux, Y, nb, k, c->log_n, ab,
                                                                c->d_info32);
       } else {
         dim3 g2(grid.x, grid.y, (unsigned)((k + 11) / 12));
-        HEFV_CUDA(cudaFuncSetAttribute(k_ksa_mac<KSA_KMAX, 12>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)dyn(KSA_KMAX, 12)));
-        k_ksa_mac<KSA_KMAX, 12><<<g2, 32 * 14, dyn(KSA_KMAX, 12), st>>>(X, kaux, Y, nb, k,
-                                                                        c->log_n, ab, c->d_info32);
+        k_ksa_mac<KSA_KMAX, 12><<<g2, 32 * 14, 0, st>>>(X, kaux, Y, nb, k, c->log_n, ab,
+                                                         c->d_info32);
       }
       HEFV_LAUNCH_CHECK("k_ksa_mac");
     }
