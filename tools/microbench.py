@@ -93,7 +93,9 @@ def main():
                     key = f"N=2^{log_n},L={L},{bits}bit,batch={batch}"
                     out["ntt"][key] = ntt_case(log_n, bits, L, batch)
             for bits in (50, 60):
-                B = max(1, min(64, (1 << 28) // (L * L * (1 << log_n) * 8)))
+                # batch: as many ciphertexts as a 256 MB scratch holds, up to 1024
+                # (small L needs large batches to fill the GPU)
+                B = max(1, min(1024, (1 << 28) // (L * L * (1 << log_n) * 8)))
                 out["keyswitch"][f"N=2^{log_n},L={L},{bits}bit,B={B}"] = ks_case(log_n, bits, L, B)
     print(json.dumps(out))
 
