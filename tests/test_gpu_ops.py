@@ -310,8 +310,9 @@ def test_ntt64_device_order_matches_oracle(log_n, bits):
     lib.hefv_ctx_destroy(h)
 
 
-@pytest.mark.parametrize("log_n", [10, 12, 13, 14, 15, 16])
-def test_ntt32_device_order_matches_oracle(log_n):
+@pytest.mark.parametrize("log_n,bits", [(10, 30), (12, 30), (13, 30), (14, 30), (15, 30),
+                                        (16, 30), (14, 28), (12, 24)])
+def test_ntt32_device_order_matches_oracle(log_n, bits):
     """Batched 30-bit device-order transforms (the persistent k_ntt32_b /
     cluster path, prime boundaries inside CTA ranges, inputs up to 2^32 - 1)
     equal the oracle's natural-order NTT permuted into bit-reversed order,
@@ -325,7 +326,7 @@ def test_ntt32_device_order_matches_oracle(log_n):
 
     n = 1 << log_n
     L, B = (3, 7) if log_n <= 14 else (2, 3)
-    primes = O.ntt_primes(L, 30, 2 * n)
+    primes = O.ntt_primes(L, bits, 2 * n)  # 28/24-bit: the Barrett input path
     psis = [root_of_unity(p, n) for p in primes]
     lib = nat.load()
     h = C.c_void_p()
