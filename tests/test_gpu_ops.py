@@ -167,6 +167,48 @@ def test_tiny_params_all_ops(rng):
         assert _digest(g.parts) == _digest(o.parts)
 
 
+@pytest.mark.parametrize("n,bits,seed", [(512, 120, 1), (1024, 240, 2), (1024, 270, 3),
+                                         (2048, 330, 4), (2048, 600, 5)])
+def test_random_op_sequences_match_oracle(n, bits, seed):
+    """Seeded random op sequences (encrypt, add, add_plain, cmult, rotations by
+    random offsets, squares and products, all_sum) over parameter sets that
+    cross the per-prime / aux-basis key-switch boundary (k = 8 | 9..20):
+    every intermediate ciphertext's limbs and level equal the oracle's."""
+    from paper_1901_10074_b200.fv import FvBackend
+
+    t = 12289  # = 1 mod 2N for every N here
+    p = BackendParams(ring_dimension=n, coeff_modulus_bits=bits, plain_modulus=t,
+                      slot_count=n // 2, depth_budget=6)
+    gpu = FvBackend(p, rng=np.random.default_rng(seed))
+    orc = O.OracleFvBackend(p, rng=np.random.default_rng(seed))
+    g = np.random.default_rng(100 + seed)
+    vecs = [g.integers(0, t, n // 2) for _ in range(3)]
+    gs = [gpu.encrypt(v) for v in vecs]
+    os_ = [orc.encrypt(v) for v in vecs]
+    for step in range(10):
+        op = g.integers(0, 6)
+        i, j = (int(x) for x in g.integers(0, len(gs), 2))
+        w = g.integers(0, t, n // 2)
+        if op == 0:
+            a, b = gpu.add(gs[i], gs[j]), orc.add(os_[i], os_[j])
+        elif op == 1:
+            a, b = gpu.add_plain(gs[i], w), orc.add_plain(os_[i], w)
+        elif op == 2:
+            a, b = gpu.cmult(gs[i], w % 17), orc.cmult(os_[i], w % 17)
+        elif op == 3:
+            off = int(g.integers(-n // 2 + 1, n // 2))
+            a, b = gpu.rotate(gs[i], off), orc.rotate(os_[i], off)
+        elif op == 4 and max(gs[i].level_used, gs[j].level_used) < 3:
+            a, b = gpu.mult(gs[i], gs[j]), orc.mult(os_[i], os_[j])
+        else:
+            a, b = gpu.all_sum(gs[i], 8), orc.all_sum(os_[i], 8)
+        assert a.level_used == b.level_used, (step, op)
+        assert _digest(a.parts) == _digest(b.parts), (step, op)
+        gs.append(a)
+        os_.append(b)
+    assert np.array_equal(gpu.decrypt(gs[-1]), orc.decrypt(os_[-1]))
+
+
 def test_desk_golden_replay_matches_reference():
     """The reference's own desk run (seed 77, 10 ops) replayed on the GPU."""
     import json
