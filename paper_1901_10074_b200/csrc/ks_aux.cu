@@ -682,9 +682,13 @@ static int run_ksa_e(hefv_ctx* c, const uint32_t* kaux, const uint32_t* dig, int
   const size_t smi = tile + (size_t)GI::N * 2 + (size_t)GI::N * 4 + 16;
   HEFV_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smf));
   HEFV_CUDA(cudaFuncSetAttribute(ki, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smi));
-  const int64_t chunk = scratch_cts < B ? scratch_cts : B;
+  // equal chunks (a full chunk plus a small remainder would leave the
+  // remainder's launches mostly tail)
+  const int64_t cap = scratch_cts < B ? scratch_cts : B;
+  const int64_t nchunks = (B + cap - 1) / cap;
+  const int64_t chunk = (B + nchunks - 1) / nchunks;
   uint32_t* X = scratch;
-  uint32_t* Y = scratch + chunk * 3 * k * n;
+  uint32_t* Y = scratch + cap * 3 * k * n;
   for (int64_t c0 = 0; c0 < B; c0 += chunk) {
     const int64_t nb = (B - c0) < chunk ? (B - c0) : chunk;
     {

@@ -103,7 +103,7 @@ def rotation_keyswitch(ctx, key, src, src_stride, slot, g, B, out0, out1, out_st
                        scratch, None, 2 * stack, adB0, adB1, adB_stride, B)
 
 
-KS_WORKSPACE_BYTES = 16 << 30  # ~1300 ciphertexts per chunk at retina (fewer kernel tails)
+KS_WORKSPACE_BYTES = 24 << 30  # ~1900 ciphertexts per chunk at retina: one chunk per config-2 launch
 
 
 def _ks_workspace(ctx, batch: int):
