@@ -38,10 +38,10 @@
 namespace hefv {
 
 #ifndef KSA_FWD_CTS_V
-#define KSA_FWD_CTS_V 8
+#define KSA_FWD_CTS_V 16
 #endif
 #ifndef KSA_INV_CTS_V
-#define KSA_INV_CTS_V 8
+#define KSA_INV_CTS_V 16
 #endif
 #ifndef KSA_MAC_CTS_V
 #define KSA_MAC_CTS_V 128
