@@ -1,11 +1,15 @@
 // Standalone batched negacyclic NTTs (K1/K2 for 30-bit primes, K3 for
-// 64-bit primes): one CTA per polynomial, the polynomial resident in
-// registers + one padded shared tile (ntt.cuh).  Replaces NttPrime.fwd/inv
-// (reference ntt.py:191-224) including the object-dtype path for p >= 2^31.
-//
-// For 64-bit primes with N > 2^14 the polynomial (>= 256 KB) does not fit a
-// CTA's shared memory; those sizes run the two-kernel global-memory variant
-// at the end of this file (column pass + row pass, each CTA-resident).
+// 64-bit primes): each polynomial resident in one CTA's registers + one
+// padded shared tile (ntt.cuh).  Replaces NttPrime.fwd/inv (reference
+// ntt.py:191-224) including the object-dtype path for p >= 2^31.
+//   * k_ntt32_b / k_ntt64_b: persistent prime-major CTAs (device order);
+//   * k_ntt_fwd / k_ntt_inv: one CTA per polynomial (natural order, small N,
+//     and the 64-bit sizes where that measured faster);
+//   * k_ntt_cl_fwd / k_ntt_cl_inv: polynomials larger than one SM (64-bit
+//     N = 2^15 / 2^16, 30-bit N = 2^16) as one thread-block cluster each,
+//     the CTA-spanning exchange through distributed shared memory;
+//   * k_ntt64_radix_pass: the four-pass global-memory fallback for 64-bit
+//     2^15 / 2^16 (HEFV_NTT64_CLUSTER=0).
 #include <cstdlib>
 
 #include "../../include/hefv.h"
