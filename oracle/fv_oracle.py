@@ -305,6 +305,47 @@ def switch_key(ctx: OracleContext, s, target, rng) -> OracleSwitchKey:
     return OracleSwitchKey(body, mask)
 
 
+def switch_key_wide(primes, n, s_rns, target_rns, rng) -> OracleSwitchKey:
+    """_keyswitch_key (fv.py:176-202) for any prime width: the same Generator
+    calls as the reference's _FvContext samplers (fv.py:114-129), the ring
+    products and the gadget scalars in object arithmetic, as the reference's
+    object-dtype path computes them for p >= 2^31."""
+    q = 1
+    for p in primes:
+        q *= p
+    gadget = [(q // p) * pow(q // p, -1, p) % q for p in primes]
+    ntts = [OracleNtt(p, n) for p in primes]
+    pcol = np.array(primes, dtype=object)[:, None]
+    k = len(primes)
+    bodies, masks = [], []
+    for i in range(k):
+        a = np.stack([rng.integers(0, p, n, dtype=np.int64) for p in primes])
+        e = np.clip(np.rint(rng.normal(0.0, SIGMA, n)).astype(np.int64), -ERR_BOUND, ERR_BOUND)
+        e = e.astype(object) % pcol
+        prod = np.stack([tr.negacyclic_mul(a[j], s_rns[j]) for j, tr in enumerate(ntts)])
+        g = np.array([gadget[i] % p for p in primes], dtype=object)[:, None]
+        body = (-((prod + e) % pcol) % pcol + np.asarray(target_rns, dtype=object) * g % pcol) % pcol
+        bodies.append(body)
+        masks.append(a.astype(object))
+    body = [tr.fwd(np.stack([bodies[i][j] for i in range(k)])) for j, tr in enumerate(ntts)]
+    mask = [tr.fwd(np.stack([masks[i][j] for i in range(k)])) for j, tr in enumerate(ntts)]
+    return OracleSwitchKey(body, mask)
+
+
+def ks64_case(primes, n, seed):
+    """Config-4 key-switch case drawn like make_golden.gen_ks64 draws it from
+    the reference: secret s (ternary), target s^2, the switch key, then the
+    input polynomial c uniform mod each prime -- one Generator."""
+    rng = np.random.default_rng(seed)
+    ntts = [OracleNtt(p, n) for p in primes]
+    pcol = np.array(primes, dtype=object)[:, None]
+    s = rng.integers(-1, 2, n, dtype=np.int64).astype(object) % pcol
+    target = np.stack([tr.negacyclic_mul(s[j], s[j]) for j, tr in enumerate(ntts)])
+    key = switch_key_wide(primes, n, s, target, rng)
+    c = np.stack([rng.integers(0, p, n, dtype=np.int64) for p in primes])
+    return key, c
+
+
 def keyswitch(ctx: OracleContext, c, key: OracleSwitchKey):
     k = len(ctx.fp.q_primes)
     d0 = np.empty((k, ctx.n), dtype=np.int64)

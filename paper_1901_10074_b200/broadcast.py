@@ -88,7 +88,7 @@ def broadcast_layer_eval(backend, rows, vals):
         # chunks so the transient copies stay small next to the layer's inputs
         x_ntt = torch.empty((len(used), 2, ctx.k, ctx.n), dtype=torch.int32, device="cuda")
         for lo in range(0, len(used), 256):
-            xin = torch.stack([vals[int(i)].device()[:2] for i in used[lo:lo + 256]])
+            xin = torch.stack([backend.dev(vals[int(i)])[:2] for i in used[lo:lo + 256]])
             x_ntt[lo:lo + 256] = ctx.to_mont(
                 ctx.ntt_q(xin.view(-1, ctx.k, ctx.n)).view_as(xin))
             del xin
@@ -147,7 +147,7 @@ def square_layer(backend, vals, release_inputs=True):
         return []
     if max(levels) > backend.params.depth_budget:
         return None
-    devs = backend._square_many_dev([ct.device() for ct in vals])
+    devs = backend._square_many_dev([backend.dev(ct) for ct in vals])
     out = [FvCiphertext(None, lv, backend.params, dev=d) for lv, d in zip(levels, devs)]
     cur = peak = freed = 0
     for ct in vals:

@@ -92,6 +92,7 @@ class FvContext:
         self.t = fp.t
         self.q_primes = list(fp.q_primes)
         self.k = len(self.q_primes)
+        self.pcol = np.array(self.q_primes, dtype=np.int64)[:, None]
         qc = CrtConstants.build(self.q_primes)
         self.q = qc.product
         self.delta = self.q // fp.t
@@ -450,10 +451,11 @@ class FvCiphertext:
         self._dev = None
 
     def device(self):
+        """The (parts, k, N) device stack.  Host parts (assigned, or read from
+        a wire record) are uploaded by ``FvBackend.dev``, which validates
+        them against the context first."""
         if self._dev is None:
-            torch = _torch()
-            stack = np.stack(self._host).astype(np.int32)
-            self._dev = nat.to_device(stack)
+            raise ParamMismatchError("host-side ciphertext parts: upload through FvBackend.dev(ct)")
         return self._dev
 
     @property
@@ -480,6 +482,14 @@ class FvBackend(SlotBackend):
         self.rng = rng if rng is not None else np.random.default_rng()
         if keys is None:
             keys = keygen(FvParams.from_backend(params), rng=self.rng)
+        elif not isinstance(keys, KeySet):
+            # the reference's host KeySet (keygen / serialize.read_keyset,
+            # fv.py:220-228): uploaded once into the device layout
+            fp = keys.context.fp
+            ctx = FvContext(FvParams(n=fp.n, t=fp.t, q_primes=list(fp.q_primes), sigma=fp.sigma))
+            keys = KeySet.from_host(ctx, keys.secret, keys.public,
+                                    (keys.relin.body, keys.relin.mask),
+                                    {off: (sk.body, sk.mask) for off, sk in keys.galois.items()})
         self.keys = keys
         self.ctx = keys.context
         if self.ctx.t != params.plain_modulus or self.ctx.n != params.ring_dimension:
@@ -489,6 +499,37 @@ class FvBackend(SlotBackend):
         self._s2_mont = ctx.to_mont(ctx.elementwise(2, keys.s_ntt, keys.s_ntt))
         self._pk_mont = ctx.to_mont(keys.pk_ntt.contiguous())
         self._e0_ntt = None
+
+    # ---- device residency -------------------------------------------------------
+    def dev(self, ct):
+        """Device stack of any ciphertext with the reference's shape: this
+        backend's handles directly; host parts (an ``FvCiphertext`` whose
+        parts were assigned, or the reference's own ``FvCiphertext`` as
+        ``serialize.read_ciphertext`` returns it, fv.py:30-42) are checked --
+        2 or 3 components of shape (k, N), every residue in [0, p_j) -- and
+        uploaded (cached on this backend's handles)."""
+        if isinstance(ct, FvCiphertext) and ct._dev is not None:
+            return ct._dev
+        parts = ct._host if isinstance(ct, FvCiphertext) else ct.parts
+        d = nat.to_device(self.check_host_parts(parts).astype(np.int32))
+        if isinstance(ct, FvCiphertext):
+            ct._dev = d
+        return d
+
+    def check_host_parts(self, parts) -> np.ndarray:
+        ctx = self.ctx
+        if len(parts) not in (2, 3):
+            raise FormatError(f"FV ciphertext needs 2 or 3 components, got {len(parts)}")
+        stack = []
+        for comp in parts:
+            arr = np.asarray(comp)
+            if arr.shape != (ctx.k, ctx.n):
+                raise FormatError(f"component shape {arr.shape} != ({ctx.k}, {ctx.n})")
+            arr = arr.astype(np.int64)
+            if (arr < 0).any() or (arr >= ctx.pcol).any():
+                raise FormatError("residue outside [0, p_j)")
+            stack.append(arr)
+        return np.stack(stack)
 
     # ---- batching ----------------------------------------------------------
     def _slots_dev(self, vecs):
@@ -594,10 +635,10 @@ class FvBackend(SlotBackend):
 
     def decrypt_poly(self, ct: FvCiphertext) -> np.ndarray:
         """Plaintext polynomial mod t (fv.py:337-349)."""
-        return self._host_plain(self._decrypt_poly_dev([ct.device()])[0])
+        return self._host_plain(self._decrypt_poly_dev([self.dev(ct)])[0])
 
     def _decrypt(self, ct):
-        slots = self._decode_dev(self._decrypt_poly_dev([ct.device()]))[0]
+        slots = self._decode_dev(self._decrypt_poly_dev([self.dev(ct)]))[0]
         return np.asarray(self._host_plain(slots), dtype=self._dtype)
 
     def decrypt_many(self, cts) -> list:
@@ -611,7 +652,7 @@ class FvBackend(SlotBackend):
             groups.setdefault(ct.nparts, []).append(i)
         res = [None] * len(cts)
         for _, idx in groups.items():
-            slots = self._decode_dev(self._decrypt_poly_dev([cts[i].device() for i in idx]))
+            slots = self._decode_dev(self._decrypt_poly_dev([self.dev(cts[i]) for i in idx]))
             host = nat.to_host(slots)
             for r, i in enumerate(idx):
                 res[i] = np.asarray(host[r] if self.ctx.t < (1 << 31) else host[r].astype(object),
@@ -619,21 +660,21 @@ class FvBackend(SlotBackend):
         return res
 
     def _add(self, a, b, level):
-        da, db = a.device(), b.device()
+        da, db = self.dev(a), self.dev(b)
         m = min(da.shape[0], db.shape[0])
         out = self.ctx.elementwise(0, da[:m].contiguous(), db[:m].contiguous())
         return self._fresh(out, level)
 
     def _add_plain(self, a, vec, level):
         dm = self._delta_m_dev(np.asarray(vec)[None])
-        da = a.device()
+        da = self.dev(a)
         out = da.clone()
         out[0] = self.ctx.elementwise(0, da[0].contiguous(), dm[0])
         return self._fresh(out, level)
 
     def _cmult(self, a, vec, level):
         m = self._cmult_plain_dev(np.asarray(vec)[None])
-        da = a.device()
+        da = self.dev(a)
         out = _torch().empty_like(da)
         self.ctx.call("hefv_mul_plain", da.data_ptr(), m.data_ptr(), out.data_ptr(), 1,
                       da.shape[0], 1, self.ctx.stream())
@@ -641,8 +682,8 @@ class FvBackend(SlotBackend):
 
     def _mult(self, a, b, level):
         ctx = self.ctx
-        da = a.device().contiguous()
-        db = da if b is a else b.device().contiguous()
+        da = self.dev(a).contiguous()
+        db = da if b is a else self.dev(b).contiguous()
         out3 = ctx.empty(3, ctx.k, ctx.n)
         scratch = ctx.empty(7 * ctx.a * ctx.n)
         ctx.call("hefv_mult_tensor", da.data_ptr(), db.data_ptr(), out3.data_ptr(),
@@ -706,7 +747,7 @@ class FvBackend(SlotBackend):
         return out
 
     def _rotate(self, a, offset, level):
-        dev = a.device()
+        dev = self.dev(a)
         if offset == 0:
             return self._fresh(dev.clone(), level)
         dev = dev[:2].contiguous()
@@ -715,6 +756,23 @@ class FvBackend(SlotBackend):
         return self._fresh(dev, level)
 
     # ---- helpers for the layer planner ---------------------------------------------
+    def layer_eval_batched(self, rows, x, skip_zero_segments=True, scale_factor=1):
+        """A whole compiled layer through the batched planner: the limbs,
+        levels, Generator draws and CostReport of the reference's per-row
+        ``layer_eval`` (inference.py:261-349).  ``rows`` / ``x`` may be the
+        reference's own ``WeightRow`` / ``PackedVector`` objects; the result
+        has the type of ``x``."""
+        from .errors import DimensionError
+        from .planner import planned_layer_eval
+
+        for row in rows:
+            if row.length != x.logical_length:
+                raise DimensionError(f"row length {row.length} != input length {x.logical_length}")
+        res = planned_layer_eval(self, rows, x, skip_zero_segments, scale_factor)
+        if type(res) is not type(x):
+            res = type(x)(res.logical_length, res.slots_used, res.cts, scale=res.scale)
+        return res
+
     def e0_plain_ntt(self):
         """Montgomery NTT of centred(encode(e0)), cached (inference.py:287, 327)."""
         if self._e0_ntt is None:

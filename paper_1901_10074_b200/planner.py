@@ -104,20 +104,40 @@ def rotation_keyswitch(ctx, key, src, src_stride, slot, g, B, out0, out1, out_st
 
 
 KS_WORKSPACE_BYTES = 24 << 30  # ~1900 ciphertexts per chunk at retina: one chunk per config-2 launch
+MEM_FRACTION = 0.3              # of the free device memory, per budget (workspace, tile)
+
+
+def _budget(limit: int, held: int = 0) -> int:
+    """``limit`` clamped to MEM_FRACTION of the device memory free now (plus
+    what the caller already holds and would give back)."""
+    import torch
+
+    free, _ = torch.cuda.mem_get_info()
+    return int(min(limit, MEM_FRACTION * (free + held)))
 
 
 def _ks_workspace(ctx, batch: int):
     """Scratch of the aux-basis key switch (9 k N words per ciphertext),
-    cached on the context; ciphertexts beyond its capacity run in chunks."""
+    cached on the context (``release_workspace`` drops it); ciphertexts
+    beyond its capacity run in chunks.  Sized from KS_WORKSPACE_BYTES and
+    the free device memory, so several live contexts do not each pin 24 GB."""
     import torch
 
     per_ct = 9 * ctx.k * ctx.n
-    cap = max(1, min(batch, KS_WORKSPACE_BYTES // (4 * per_ct)))
     ws = getattr(ctx, "_ks_ws", None)
+    held = 0 if ws is None else ws.numel() * 4
+    if ws is not None and ws.numel() >= min(batch, KS_WORKSPACE_BYTES // (4 * per_ct)) * per_ct:
+        return ws, ws.numel() // per_ct
+    cap = max(1, min(batch, _budget(KS_WORKSPACE_BYTES, held) // (4 * per_ct)))
     if ws is None or ws.numel() < cap * per_ct:
-        ctx._ks_ws = None
+        ws = ctx._ks_ws = None      # the old buffer is freed before the new one is allocated
         ws = ctx._ks_ws = torch.empty(cap * per_ct, dtype=torch.int32, device="cuda")
     return ws, ws.numel() // per_ct
+
+
+def release_workspace(ctx) -> None:
+    """Drop the key-switch workspace cached on ``ctx``."""
+    ctx._ks_ws = None
 
 
 def count_layer_ops(rows, x_k: int, s: int, slot_count: int, galois_offsets,
@@ -339,7 +359,7 @@ def _tile_rows(backend, n_plain_per_row: float) -> int:
     ctx = backend.ctx
     ct_bytes = 2 * ctx.k * ctx.n * 4
     per_row = 2 * ct_bytes + n_plain_per_row * (ctx.k * ctx.n * 4 + ctx.n * 8)
-    return int(max(1, min(8192, _TILE_BYTES // per_row)))
+    return int(max(1, min(8192, _budget(_TILE_BYTES) // per_row)))
 
 
 def _run_rows(backend, rows, x, seg_lists, active, m_arr, off_arr, bias_arr, out_dev, n_iter,
@@ -354,7 +374,7 @@ def _run_rows(backend, rows, x, seg_lists, active, m_arr, off_arr, bias_arr, out
     stack = kq * n
     ct_words = 2 * stack
     # NTT (device order, Montgomery form) of the layer inputs, once per layer
-    xin = torch.stack([ct.device()[:2] for ct in x.cts]).contiguous()
+    xin = torch.stack([backend.dev(ct)[:2] for ct in x.cts]).contiguous()
     x_ntt = ctx.to_mont(ctx.ntt_q(xin.view(-1, kq, n)).view_as(xin))
 
     # rows grouped by output ciphertext (stable), so each tile's pieces are contiguous per m

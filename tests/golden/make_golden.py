@@ -341,3 +341,240 @@ def gen_matrix():
 
 if __name__ == "__main__" and "--matrix" in sys.argv:
     gen_matrix()
+
+
+# ---- sharded reference: whole-layer limb goldens at retina ----------------
+#
+# The reference evaluates a layer one row at a time (inference.py:261-349);
+# every row's piece is added into its output ciphertext, and limb-wise
+# addition mod p_j is exact and commutative.  So a layer restricted to a row
+# subset R (the other rows replaced by all-zero rows, which layer_eval skips
+# without any operation, inference.py:303-309) splits into shards R_1..R_W
+# whose outputs sum limb-wise to the output over R -- provided every shard
+# places at least one row in every output ciphertext (otherwise layer_eval
+# encrypts a fresh zero there, inference.py:339-341).  Each worker runs the
+# unmodified reference (own keygen from default_rng(1234), so identical keys
+# and input encryptions) on its shard; the parent sums the pieces mod p_j,
+# then runs the reference's own square (and, for config 2, the FC layer) on
+# the summed ciphertexts.  Digests of all of it go to rows_shard_c{2,3}.json.
+
+SHARD_WORKERS = 8
+
+
+def _popcount(x):
+    return bin(x).count("1")
+
+
+def rows_shard_picks(cfg):
+    """Deterministic row picks (out_index values) and their shard split.
+
+    Config 2 (10,580 conv rows, 2 output cts): every placement-hop count
+    1..13 (rotation by -off = 8192-off, popcount hops, fv.py:422-425) in both
+    output ciphertexts where it exists, off = 0, the rows whose 5x5 window
+    straddles the input-ciphertext boundary (image rows 85/86 -> oy 41, 42)
+    for every filter, first / last rows, and seeded random rows -> 64.
+    Config 3 (rows list truncated to the first 16,384 conv1 rows = filter 0
+    and the start of filter 1, 2 output cts): every row spans 3 channels
+    (3-6 input segments); picks cover the input-ct boundary rows (input ct =
+    32 image rows: oy 14, 15, 16 and 30, 31), placement hop counts, and the
+    filter-0/1 boundary -> 32."""
+    s = 8192
+    if cfg == 2:
+        total, f_len, ow, want = 10580, 2116, 46, 64
+        picks = {0, s, total - 1, 1}
+        for b in range(1, 14):
+            for ct in (0, 1):
+                lim = s if ct == 0 else total - s
+                cands = [off for off in range(1, lim) if _popcount(s - off) == b]
+                if cands:
+                    picks.add(ct * s + cands[len(cands) // 2])
+        for f in range(5):
+            for oy in (41, 42):
+                picks.add(f * f_len + oy * ow + 7 * f)
+    else:
+        total, f_len, ow, want = 16384, 15876, 126, 32
+        picks = {0, s, total - 1, 8191, f_len - 1, f_len}
+        for oy in (14, 15, 16, 30, 31, 62, 64):
+            picks.add(oy * ow + (oy * 3) % ow)
+        for b in (1, 4, 8, 11, 13):
+            cands = [off for off in range(1, total - s) if _popcount(s - off) == b]
+            if cands:
+                picks.add(s + cands[len(cands) // 3])
+    rng = np.random.default_rng(20 + cfg)
+    while len(picks) < want:
+        picks.add(int(rng.integers(0, total)))
+    picks = sorted(picks)[:want] if len(picks) > want else sorted(picks)
+    ct0 = [r for r in picks if r < s]
+    ct1 = [r for r in picks if r >= s]
+    assert len(ct1) >= SHARD_WORKERS and len(ct0) >= SHARD_WORKERS, (len(ct0), len(ct1))
+    shards = [[] for _ in range(SHARD_WORKERS)]
+    for i, r in enumerate(ct0):
+        shards[i % SHARD_WORKERS].append(r)
+    for i, r in enumerate(ct1):
+        shards[i % SHARD_WORKERS].append(r)
+    return total, picks, [sorted(sh) for sh in shards]
+
+
+def _shard_setup(cfg):
+    if cfg == 2:
+        p = profile("retina")
+        img, net = net_for(2)
+        conv = net.layers[0]
+    else:
+        p = profile("retina").replace(coeff_modulus_bits=720)
+        rng = np.random.default_rng(3)
+        img = rng.integers(0, 256, (3, 256, 256), dtype=np.int64)
+        conv = R_inf.ConvSpec(8, (5, 5), (2, 2), (3, 256, 256), rng.integers(-8, 9, (8, 3, 5, 5)),
+                              np.zeros(8, np.int64))
+        net = None
+    return p, img, net, conv
+
+
+def _masked_rows(rows, keep, total):
+    out = []
+    keep = set(keep)
+    for i in range(total):
+        r = rows[i]
+        if i in keep:
+            out.append(r)
+        else:
+            out.append(R_inf.WeightRow(out_index=r.out_index, length=r.length,
+                                       slots_used=r.slots_used,
+                                       positions=np.zeros(0, np.int64),
+                                       values=np.zeros(0, np.int64), bias=0))
+    return out
+
+
+def _shard_worker(args):
+    cfg, shard = args
+    p, img, net, conv = _shard_setup(cfg)
+    t0 = time.time()
+    be = R_fv.FvBackend(p, rng=np.random.default_rng(1234))
+    pv = R_inf.pack_image(be, img)
+    total, _, _ = rows_shard_picks(cfg)
+    rows = R_inf.compile_conv(conv, pv.slots_used)
+    res = R_inf.layer_eval(be, _masked_rows(rows, shard, total), pv)
+    return {"parts": [[np.asarray(x, dtype=np.int64) for x in ct.parts] for ct in res.cts],
+            "levels": [ct.level_used for ct in res.cts],
+            "cost": be.cost_report().as_dict(), "seconds": time.time() - t0,
+            "enc": [digest(ct.parts) for ct in pv.cts]}
+
+
+def gen_rows_shard(cfg):
+    import multiprocessing as mp
+
+    total, picks, shards = rows_shard_picks(cfg)
+    t0 = time.time()
+    import pickle
+
+    cache = Path(f"/tmp/rows_shard_c{cfg}.pkl")   # scratch: reruns skip the shards
+    if cache.exists():
+        outs = pickle.loads(cache.read_bytes())
+    else:
+        with mp.get_context("fork").Pool(SHARD_WORKERS) as pool:
+            outs = pool.map(_shard_worker, [(cfg, sh) for sh in shards])
+        cache.write_bytes(pickle.dumps(outs))
+    p, img, net, conv = _shard_setup(cfg)
+    fp = R_fv.FvParams.from_backend(p)
+    q = [int(x) for x in fp.q_primes]
+    qcol = np.asarray(q, dtype=np.int64)[:, None]
+    n_out = len(outs[0]["parts"])
+    summed = []
+    for m in range(n_out):
+        parts = []
+        for c in range(2):
+            acc = np.zeros_like(outs[0]["parts"][m][c])
+            for o in outs:
+                acc = (acc + o["parts"][m][c]) % qcol
+            parts.append(acc)
+        summed.append(parts)
+    out = {"config": cfg, "key_seed": 1234, "total_rows": total, "picks": picks,
+           "shards": shards, "workers": SHARD_WORKERS,
+           "shard_enc": outs[0]["enc"],
+           "shard_levels": outs[0]["levels"],
+           "shard_costs": [o["cost"] for o in outs],
+           "shard_seconds": [o["seconds"] for o in outs],
+           "conv_out": [digest(parts) for parts in summed]}
+    assert all(o["enc"] == outs[0]["enc"] for o in outs)
+    # the reference's own square (and FC) on the summed layer output
+    be = R_fv.FvBackend(p, rng=np.random.default_rng(1234))
+    pv = R_inf.pack_image(be, img)
+    assert [digest(ct.parts) for ct in pv.cts] == outs[0]["enc"]
+    lvl = outs[0]["levels"][0]
+    cts = [R_fv.FvCiphertext([np.asarray(x) for x in parts], lvl, be.params)
+           for parts in summed]
+    x = R_inf.PackedVector(total, pv.slots_used, cts)
+    t1 = time.time()
+    sq = R_inf.square_activation(be, x)
+    out["square_out"] = [digest(ct.parts) for ct in sq.cts]
+    out["square_levels"] = [ct.level_used for ct in sq.cts]
+    if cfg == 2:
+        fc = net.layers[2]
+        rows = R_inf.compile_fc(fc, sq.slots_used)
+        res = R_inf.layer_eval(be, rows, sq)
+        out["fc_out"] = [digest(ct.parts) for ct in res.cts]
+        out["fc_levels"] = [ct.level_used for ct in res.cts]
+        out["logits"] = [int(v) for v in R_inf.decrypt_logits(be, res)]
+        # the same square / FC over the summed input, decrypted slot values
+        out["square_dec_digest"] = [vec_digest(be.decrypt(ct)) for ct in sq.cts]
+    out["tail_seconds"] = time.time() - t1
+    out["seconds"] = time.time() - t0
+    dump(f"rows_shard_c{cfg}.json", out)
+
+
+if __name__ == "__main__" and "--rows-shard" in sys.argv:
+    for c in (2, 3):
+        if f"--c{c}" in sys.argv or not any(f"--c{x}" in sys.argv for x in (2, 3)):
+            gen_rows_shard(c)
+
+
+# ---- config 4: the 50-62-bit key switch, run by the reference -------------
+KS64_CASES = [(4096, 2), (4096, 4), (4096, 8), (16384, 2), (16384, 4), (16384, 8), (65536, 2)]
+
+
+def _ks64_one(args):
+    n, L = args
+    primes = R_ntt.find_ntt_primes(L, 60, 2 * n)
+    t = R_ntt.find_ntt_primes(1, 20, 2 * n)[0]
+    ctx = R_fv._FvContext(R_fv.FvParams(n=n, t=t, q_primes=primes))
+    seed = 4000 + n + L
+    rng = np.random.default_rng(seed)
+    t0 = time.time()
+    s = ctx.to_rns(ctx.rand_ternary(rng))
+    key = R_fv._keyswitch_key(ctx, s, ctx.mul(s, s), rng)
+    c = ctx.rand_uniform(rng)
+    t1 = time.time()
+    d0, d1 = R_fv._keyswitch_apply(ctx, c, key)
+    t2 = time.time()
+    return {"n": n, "L": L, "bits": 60, "primes": primes, "t": t, "seed": seed,
+            "key": key_digest(key), "c": digest([c]), "d0": digest([d0]), "d1": digest([d1]),
+            "keygen_seconds": t1 - t0, "apply_seconds": t2 - t1}
+
+
+def gen_ks64():
+    """Reference _keyswitch_key + _keyswitch_apply (fv.py:176-217) over
+    _FvContext(FvParams(n, t, 60-bit primes)) -- the object-dtype path."""
+    import multiprocessing as mp
+
+    with mp.get_context("fork").Pool(len(KS64_CASES)) as pool:
+        cases = pool.map(_ks64_one, KS64_CASES)
+    dump("ks64.json", {"cases": cases})
+
+
+if __name__ == "__main__" and "--ks64" in sys.argv:
+    gen_ks64()
+
+
+def gen_config5_enc_impl(count=3, image_seed=5):
+    """Config 5: the first images of the stream (configs.batch_images: one
+    default_rng(5) drawing (1, 96, 96) images in turn) encrypted in sequence
+    under one key -- one Generator for keygen and every encryption."""
+    rng = np.random.default_rng(image_seed)
+    imgs = [rng.integers(0, 256, (1, 96, 96), dtype=np.int64) for _ in range(count)]
+    be = R_fv.FvBackend(profile("retina"), rng=np.random.default_rng(1234))
+    enc = [[digest(ct.parts) for ct in R_inf.pack_image(be, img).cts] for img in imgs]
+    dump("config5_enc.json", {"key_seed": 1234, "image_seed": image_seed, "enc": enc})
+
+
+if __name__ == "__main__" and "--config5" in sys.argv:
+    gen_config5_enc_impl()

@@ -229,15 +229,3 @@ def test_gpu_keyset_rejects_other_params(tmp_path):
     with pytest.raises(ParamMismatchError):
         FvBackend(params.replace(plain_modulus=40961), keys=loaded)
 
-
-def test_enc_matrix_roundtrip(tmp_path, desk, rng):
-    from paper_1901_10074_b200.matrix import Layout, PlainMatrix, pack_matrix, unpack_matrix
-    from paper_1901_10074_b200.serialize import read_enc_matrix, write_enc_matrix
-
-    m = PlainMatrix(3, 5, rng.integers(0, 100, (3, 5)))
-    enc = pack_matrix(desk, m, Layout.CCP, slots_used=8)
-    path = tmp_path / "mat.bin"
-    write_enc_matrix(path, enc, desk.params)
-    again = read_enc_matrix(path, desk)
-    assert (again.rows, again.cols, again.layout, again.slots_used) == (3, 5, Layout.CCP, 8)
-    assert np.array_equal(unpack_matrix(desk, again).entries, unpack_matrix(desk, enc).entries)
