@@ -65,6 +65,12 @@ int hefv_ntt_fwd64(hefv_ctx* ctx, const uint64_t* in, uint64_t* out, int64_t bat
 int hefv_ntt_inv64(hefv_ctx* ctx, const uint64_t* in, uint64_t* out, int64_t batch,
                    int32_t nprimes, int32_t prime_base, int32_t natural, void* stream);
 
+/* Pointwise product of canonical residue rows: out = a * b mod p, data
+ * (batch, nprimes, N) as above (words of 4 bytes, or 8 when wide = 1).
+ * The middle step of NttPrime.negacyclic_mul (ntt.py:226-227). */
+int hefv_pointwise_mul(hefv_ctx* ctx, int32_t wide, const void* a, const void* b, void* out,
+                       int64_t batch, int32_t nprimes, int32_t prime_base, void* stream);
+
 /* ---- FV layer setup ------------------------------------------------------
  * k q-primes = 32-bit primes [0, k), a auxiliary primes = [k, k + a),
  * t = 64-bit prime t_index.  slot_to_ev: (N/2) natural evaluation index of

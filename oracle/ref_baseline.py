@@ -115,19 +115,22 @@ def sample(state, hops=1, cmults=1, adds=10) -> dict:
     """Per-op seconds of the reference's own operations on this core."""
     be, vec, ct = state["be"], state["vec"], state["ct"]
     res = {}
-    c = time.perf_counter()
     cur = ct
-    for _ in range(hops):
-        cur = be.rotate(cur, 1)          # one hop: Galois key for offset 1 exists
-    res["ks_hop"] = (time.perf_counter() - c) / hops
-    c = time.perf_counter()
-    for _ in range(cmults):
-        be.cmult(ct, vec)
-    res["cmult"] = (time.perf_counter() - c) / cmults
-    c = time.perf_counter()
-    for _ in range(adds):
-        be.add(ct, cur)
-    res["add"] = (time.perf_counter() - c) / adds
+    if hops:
+        c = time.perf_counter()
+        for _ in range(hops):
+            cur = be.rotate(cur, 1)      # one hop: a Galois key for offset 1 exists
+        res["ks_hop"] = (time.perf_counter() - c) / hops
+    if cmults:
+        c = time.perf_counter()
+        for _ in range(cmults):
+            be.cmult(ct, vec)
+        res["cmult"] = (time.perf_counter() - c) / cmults
+    if adds:
+        c = time.perf_counter()
+        for _ in range(adds):
+            be.add(ct, cur)
+        res["add"] = (time.perf_counter() - c) / adds
     return res
 
 

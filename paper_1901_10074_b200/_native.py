@@ -30,6 +30,7 @@ _SIGS = {
     "hefv_ntt_inv32": [_P, _P, _P, _I64, _I32, _I32, _I32, _P],
     "hefv_ntt_fwd64": [_P, _P, _P, _I64, _I32, _I32, _I32, _P],
     "hefv_ntt_inv64": [_P, _P, _P, _I64, _I32, _I32, _I32, _P],
+    "hefv_pointwise_mul": [_P, _I32, _P, _P, _P, _I64, _I32, _I32, _P],
     "hefv_fv_setup": [_P, _I32, _I32, _I32, _P, _I32, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P],
     "hefv_encode": [_P, _P, _P, _I64, _P],
     "hefv_decode": [_P, _P, _P, _I64, _P],

@@ -103,10 +103,6 @@ int hefv_ctx_create(hefv_ctx** out, uint32_t log_n, int32_t n32, const uint32_t*
   if (log_n < 1 || log_n > 16) return fail("hefv_ctx_create: log_n must be in [1, 16]");
   if (n32 < 0 || n64 < 0 || n32 + n64 == 0) return fail("hefv_ctx_create: empty prime set");
   hefv_ctx* c = new hefv_ctx();
-  if (const char* v = std::getenv("HEFV_KS_TMEM")) c->ks_tmem = std::atoi(v);
-  if (const char* v = std::getenv("HEFV_KS_E32")) c->ks_e32 = std::atoi(v);
-  if (const char* v = std::getenv("HEFV_KS_PREFETCH")) c->ks_prefetch = std::atoi(v);
-  if (const char* v = std::getenv("HEFV_KSA_MAC24")) c->ksa_mac24 = std::atoi(v);
   c->log_n = (int)log_n;
   c->n = 1 << log_n;
   const int n = c->n;
@@ -244,7 +240,10 @@ int hefv_fv_setup(hefv_ctx* c, int32_t k, int32_t a, int32_t t_index, const int3
   if (!c) return fail("hefv_fv_setup: null context");
   if (k < 1 || a < 0 || k + a > c->n32) return fail("hefv_fv_setup: prime counts exceed context");
   if (t_index < 0 || t_index >= c->n64) return fail("hefv_fv_setup: bad t_index");
-  if (wq < 1 || wq > 32) return fail("hefv_fv_setup: q must have 1..32 words");
+  // the exact t/q roundings divide by q with Knuth's algorithm D, which needs a
+  // normalised divisor of at least two words (q >= 2^32: two or more q primes,
+  // as FvParams.from_backend always chooses)
+  if (wq < 2 || wq > 32) return fail("hefv_fv_setup: q must have 2..32 32-bit words (q >= 2^32)");
   if (wm > 64) return fail("hefv_fv_setup: aux product must have <= 64 words");
   for (int j = 0; j < k + a; ++j) {
     if (c->primes32[j] <= (1u << 28))

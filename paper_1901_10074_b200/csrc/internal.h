@@ -60,10 +60,6 @@ struct hefv_ctx {
   int q_shift = 0;     // normalisation shift of q for long division
   uint32_t* d_delta = nullptr;   // Delta mod q_j (k)
   uint32_t* d_tmod = nullptr;    // t mod q_j (k)
-  int ks_prefetch = 0;  // key switch: bulk-copy prefetch of the next digit into the tile (measured slower)
-  int ks_e32 = 0;   // key switch at N = 2^14: 32 words per thread (512 threads)
-  int ks_tmem = 0;
-  int ksa_mac24 = 1;  // aux key switch, 22 < k <= 24: one 24-warp MAC CTA (HEFV_KSA_MAC24=0: two 12-warp CTAs)
   // aux-basis key switch (hefv_ks_aux_setup): three ~28-bit NTT primes at
   // primes32[ksa_base, ksa_base + 3)
   bool ksa_ready = false;

@@ -33,7 +33,6 @@
 #include "internal.h"
 #include "kcommon.cuh"
 #include "ntt.cuh"
-#include "tmem.cuh"
 
 namespace hefv {
 
@@ -642,23 +641,8 @@ static int run_ksa(hefv_ctx* c, const uint32_t* kaux, const uint32_t* dig, int64
                    const uint32_t* a0, const uint32_t* a1, int64_t as, const uint32_t* b0,
                    const uint32_t* b1, int64_t bs, uint32_t* scratch, int64_t scratch_cts,
                    int64_t B, cudaStream_t st) {
-  // transform geometry: 16 words per thread by default; HEFV_KSA_E32 = 1 / 2
-  // / 3 selects 32 words per thread (512 threads) for fwd / inv / both at 2^14
-  if constexpr (LOGN == 14) {
-    static const int e32 = [] {
-      const char* v = getenv("HEFV_KSA_E32");
-      return v ? atoi(v) : 0;
-    }();
-    if (e32 == 1)
-      return run_ksa_e<LOGN, 5, 4>(c, kaux, dig, ds, dslot, ginv, o0, o1, os, slot, a0, a1, as, b0, b1, bs,
-                                   scratch, scratch_cts, B, st);
-    if (e32 == 2)
-      return run_ksa_e<LOGN, 4, 5>(c, kaux, dig, ds, dslot, ginv, o0, o1, os, slot, a0, a1, as, b0, b1, bs,
-                                   scratch, scratch_cts, B, st);
-    if (e32 == 3)
-      return run_ksa_e<LOGN, 5, 5>(c, kaux, dig, ds, dslot, ginv, o0, o1, os, slot, a0, a1, as, b0, b1, bs,
-                                   scratch, scratch_cts, B, st);
-  }
+  // transform geometry: 16 words per thread (32 per thread at 512 threads was
+  // measured slower for both phases)
   return run_ksa_e<LOGN, 4, 4>(c, kaux, dig, ds, dslot, ginv, o0, o1, os, slot, a0, a1, as, b0, b1, bs,
                                scratch, scratch_cts, B, st);
 }
@@ -716,7 +700,7 @@ static int run_ksa_e(hefv_ctx* c, const uint32_t* kaux, const uint32_t* dig, int
                                                                c->d_info32);
       } else if (k <= 16) {
         k_ksa_mac<16, 16><<<grid, 32 * 18, 0, st>>>(X, kaux, Y, nb, k, c->log_n, ab, c->d_info32);
-      } else if (k > 22 && c->ksa_mac24) {
+      } else if (k > 22) {
         HEFV_CUDA(cudaFuncSetAttribute(k_ksa_mac<24, 24>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)dyn(24, 24)));

@@ -20,7 +20,6 @@
 #include "internal.h"
 #include "kcommon.cuh"
 #include "ntt.cuh"
-#include "tmem.cuh"
 
 namespace hefv {
 
@@ -44,11 +43,7 @@ constexpr int KS_CTS_PER_CTA = HEFV_KS_CTS;
 // [register e][thread] so every thread touches its own conflict-free words).
 // The body accumulator acc0 and the digit being transformed stay in
 // registers (2 E words per thread).
-// PREFETCH: the next digit limb is streamed into the exchange tile with a
-// bulk async copy (cp.async.bulk -> mbarrier) as soon as the current forward
-// transform has finished with the tile, so its L2/HBM latency hides behind
-// the last pass and the MAC.
-template <int LOGN, int LOGE, bool PREFETCH = false>
+template <int LOGN, int LOGE>
 __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT,
                                   Geo<LOGN, LOGE>::NT >= 1024 ? 1 : 1024 / Geo<LOGN, LOGE>::NT)
     k_keyswitch(const uint32_t* __restrict__ kbody, const uint32_t* __restrict__ kmask,
@@ -70,7 +65,6 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT,
   uint2* tws = reinterpret_cast<uint2*>(smraw);
   uint32_t* sm = reinterpret_cast<uint32_t*>(tws + NTW);  // exchange tile
   uint32_t* acc1s = sm + ((spad_size(N) + 3) & ~3);      // mask accumulator (16B aligned)
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(acc1s + N);
   const int j = blockIdx.x;
   const int tid = threadIdx.x;
   const Prime32Info inf = info[j];
@@ -92,15 +86,6 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT,
   // cover 128 consecutive bytes (conflict-free)
   uint4* acc1v = reinterpret_cast<uint4*>(acc1s);
   const Mod32M mm{inf.p, 2 * inf.p, inf.pinv};
-  uint32_t phase = 0;
-  if constexpr (PREFETCH) {
-    if (tid == 0) {
-      mbar_init(mbar, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (tid == 0) bulk_g2s(sm, digits + bbeg * dig_stride, N * 4, mbar);
-  }
   for (int64_t b = bbeg; b < bend; ++b) {
     const uint32_t* dig = digits + b * dig_stride;
     uint32_t acc0[E], x[E];
@@ -110,25 +95,12 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT,
     for (int q = 0; q < E / 4; ++q) acc1v[q * NT + tid] = make_uint4(0u, 0u, 0u, 0u);
 
     for (int i = 0; i < k; ++i) {
-      if constexpr (PREFETCH) {
-        mbar_wait(mbar, phase);
-        phase ^= 1u;
-#pragma unroll
-        for (int e = 0; e < E; ++e) x[e] = sm[tid + e * NT];
-      } else {
+      {
         const uint32_t* src = dig + (size_t)i * N;
 #pragma unroll
         for (int e = 0; e < E; ++e) x[e] = ld_stream(src + tid + e * NT);
       }
       cta_fwd<LOGN, LOGE, Mod32>(md, x, sm, tws, twg, NoHook(), LOGN - R);
-      if constexpr (PREFETCH) {
-        if (i + 1 < k) {
-          // every thread is done with the tile: stream the next limb into it
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          __syncthreads();
-          if (tid == 0) bulk_g2s(sm, dig + (size_t)(i + 1) * N, N * 4, mbar);
-        }
-      }
       const size_t koff = ((size_t)j * k + i) * N + row_index<LOGN, LOGE>(tid, 0);
       const uint4* kb = reinterpret_cast<const uint4*>(kbody + koff);
       const uint4* km = reinterpret_cast<const uint4*>(kmask + koff);
@@ -178,186 +150,7 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT,
         o[idx] = v;
       }
     }
-    if constexpr (PREFETCH) {
-      if (b + 1 < bend) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();
-        if (tid == 0) bulk_g2s(sm, digits + (b + 1) * dig_stride, N * 4, mbar);
-      }
-    }
   }
-}
-
-// ---------------------------------------------------------------------------
-// TMEM / bulk-copy variant (N >= 2^11 with 16 words per thread):
-//   * the mask accumulator lives in Tensor Memory: warp w owns TMEM lanes
-//     32 (w mod 4) .. +31 and 16 columns at 16 (w / 4); each digit's update is
-//     one tcgen05.ld / tcgen05.st of 16 columns per thread;
-//   * digit limbs are streamed by cp.async.bulk into a shared staging buffer,
-//     the next one issued as soon as every thread has consumed the current
-//     one, so the L2 latency of each 64 KB limb is hidden behind a transform;
-//   * shared memory: Shoup twiddles of every stage but the last (N/2 entries),
-//     the padded exchange tile and the staging buffer.
-// ---------------------------------------------------------------------------
-template <int LOGN, int LOGE, bool ACC0_TMEM>
-__global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
-    k_keyswitch_tm(const uint32_t* __restrict__ kbody, const uint32_t* __restrict__ kmask,
-                   const uint32_t* __restrict__ digits, int64_t dig_stride, uint32_t* out0,
-                   uint32_t* out1, int64_t out_stride, const int32_t* __restrict__ slot,
-                   const uint32_t* __restrict__ adA0, const uint32_t* __restrict__ adA1,
-                   int64_t adA_stride, const uint32_t* adB0, const uint32_t* adB1,
-                   int64_t adB_stride, int64_t B, int k, const uint2* __restrict__ tw_all,
-                   const uint2* __restrict__ itw_all, const Prime32Info* __restrict__ info) {
-  typedef Geo<LOGN, LOGE> G_;
-  constexpr int E = G_::E;
-  constexpr int NT = G_::NT;
-  constexpr int N = G_::N;
-  constexpr int NTW = N / 2;  // twiddles of stages 0 .. LOGN-2
-  constexpr int TILE = (spad_size(N) + 3) & ~3;
-  constexpr uint32_t ACOLS = (uint32_t)(N / 128);              // columns per accumulator
-  constexpr uint32_t NEED = ACC0_TMEM ? 2 * ACOLS : ACOLS;
-  constexpr uint32_t TCOLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
-  static_assert(E % 16 == 0, "TMEM accumulators move 16 columns at a time");
-  extern __shared__ __align__(16) unsigned char smraw[];
-  uint2* tws = reinterpret_cast<uint2*>(smraw);
-  uint32_t* sm = reinterpret_cast<uint32_t*>(tws + NTW);
-  uint32_t* stage = sm + TILE;                                  // N words, 16B aligned
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(stage + N);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 1);
-  const int j = blockIdx.x;
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5;
-  const Prime32Info inf = info[j];
-  const Mod32 md{inf.p, 2 * inf.p};
-  const Mod32M mm{inf.p, 2 * inf.p, inf.pinv};
-  const uint2* twg = tw_all + (size_t)j * N;
-  const uint2* itw = itw_all + (size_t)j * N;
-  const int64_t bbeg = (int64_t)blockIdx.y * KS_CTS_PER_CTA;
-  const int64_t bend = min(B, bbeg + KS_CTS_PER_CTA);
-
-  if (tid == 0) mbar_init(mbar, 1);
-  if (warp == 0) tmem_alloc(tslot, TCOLS);
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(twg);
-    uint4* dst = reinterpret_cast<uint4*>(tws);
-    for (int i = tid; i < NTW / 2; i += NT) dst[i] = __ldg(src + i);
-  }
-  tmem_fence_before();
-  __syncthreads();
-  tmem_fence_after();
-  const uint32_t tbase = *tslot;
-  // warp w: TMEM lanes 32 (w mod 4) .. +31, columns E (w / 4) .. +E-1 (acc1 at
-  // +ACOLS when both accumulators live in TMEM)
-  const uint32_t tacc1 =
-      tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(E * (warp >> 2));
-  const uint32_t tacc0 = tacc1 + ACOLS;
-  uint32_t phase = 0;
-  if (tid == 0) bulk_g2s(stage, digits + bbeg * dig_stride, N * 4, mbar);
-
-  for (int64_t b = bbeg; b < bend; ++b) {
-    uint32_t x[E];
-    uint32_t acc0r[ACC0_TMEM ? 1 : E];
-    {
-      uint32_t z[16];
-#pragma unroll
-      for (int e = 0; e < 16; ++e) z[e] = 0u;
-#pragma unroll
-      for (int h = 0; h < E / 16; ++h) {
-        tmem_st16(tacc1 + 16 * h, z);
-        if constexpr (ACC0_TMEM) tmem_st16(tacc0 + 16 * h, z);
-      }
-      if constexpr (!ACC0_TMEM) {
-#pragma unroll
-        for (int e = 0; e < E; ++e) acc0r[e] = 0u;
-      }
-      tmem_wait_st();
-    }
-
-    for (int i = 0; i < k; ++i) {
-      mbar_wait(mbar, phase);
-      phase ^= 1u;
-#pragma unroll
-      for (int e = 0; e < E; ++e) x[e] = stage[tid + e * NT];
-      const uint32_t* nxt = nullptr;
-      if (i + 1 < k)
-        nxt = digits + b * dig_stride + (size_t)(i + 1) * N;
-      else if (b + 1 < bend)
-        nxt = digits + (b + 1) * dig_stride;
-      auto hook = [&]() {
-        if (tid == 0 && nxt) bulk_g2s(stage, nxt, N * 4, mbar);
-      };
-      cta_fwd<LOGN, LOGE, Mod32>(md, x, sm, tws, twg, hook, LOGN - G_::RLAST);
-      const size_t koff = ((size_t)j * k + i) * N + row_index<LOGN, LOGE>(tid, 0);
-      const uint4* kb = reinterpret_cast<const uint4*>(kbody + koff);
-      const uint4* km = reinterpret_cast<const uint4*>(kmask + koff);
-#pragma unroll
-      for (int h = 0; h < E / 16; ++h) {
-        uint32_t a1[16], a0t[16];
-        tmem_ld16(tacc1 + 16 * h, a1);
-        if constexpr (ACC0_TMEM) tmem_ld16(tacc0 + 16 * h, a0t);
-        tmem_wait_ld();
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint4 wb = ld_stream_v4(kb + 4 * h + q);
-          const uint4 wm = ld_stream_v4(km + 4 * h + q);
-          const uint32_t kbv[4] = {wb.x, wb.y, wb.z, wb.w};
-          const uint32_t kmv[4] = {wm.x, wm.y, wm.z, wm.w};
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            const int e = 16 * h + q * 4 + r;
-            const int l = q * 4 + r;
-            if constexpr (ACC0_TMEM) {
-              a0t[l] = md.sub2p(a0t[l] + mm.mul(x[e], kbv[r]));
-            } else {
-              acc0r[e] = md.sub2p(acc0r[e] + mm.mul(x[e], kbv[r]));
-            }
-            a1[l] = md.sub2p(a1[l] + mm.mul(x[e], kmv[r]));
-          }
-        }
-        tmem_st16(tacc1 + 16 * h, a1);
-        if constexpr (ACC0_TMEM) tmem_st16(tacc0 + 16 * h, a0t);
-      }
-      tmem_wait_st();
-    }
-
-    const int64_t s = slot ? (int64_t)slot[b] : b;
-#pragma unroll 1
-    for (int part = 0; part < 2; ++part) {
-      if (part == 1 || ACC0_TMEM) {
-        const uint32_t ta = part ? tacc1 : tacc0;
-#pragma unroll
-        for (int h = 0; h < E / 16; ++h) tmem_ld16(ta + 16 * h, x + 16 * h);
-        tmem_wait_ld();
-      } else {
-#pragma unroll
-        for (int e = 0; e < E; ++e) x[e] = acc0r[e];
-      }
-      cta_inv<LOGN, LOGE, Mod32>(md, x, sm, itw, inf.ninv, inf.wn);
-      uint32_t* o = (part ? out1 : out0) + s * out_stride + (size_t)j * N;
-      const uint32_t* aA = part ? adA1 : adA0;
-      const uint32_t* aB = part ? adB1 : adB0;
-      const uint32_t* a = aA ? aA + b * adA_stride + (size_t)j * N : nullptr;
-      const uint32_t* c = aB ? aB + s * adB_stride + (size_t)j * N : nullptr;
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int idx = tid + e * NT;
-        uint32_t v = md.subp(x[e]);
-        if (a) v = md.subp(v + a[idx]);
-        if (c) v = md.subp(v + c[idx]);
-        o[idx] = v;
-      }
-    }
-  }
-  tmem_fence_before();
-  __syncthreads();
-  tmem_fence_after();
-  if (warp == 0) tmem_dealloc(tbase, TCOLS);
-}
-
-template <int LOGN>
-constexpr size_t ks_tm_smem() {
-  return (size_t)(1 << (LOGN - 1)) * sizeof(uint2) +
-         (size_t)(((spad_size(1 << LOGN) + 3) & ~3) + (1 << LOGN)) * 4 + 16 + 16;
 }
 
 template <int LOGN, int LE>
@@ -371,35 +164,6 @@ static int run_ks(hefv_ctx* c, const uint32_t* kb, const uint32_t* km, const uin
                   int64_t ds, uint32_t* o0, uint32_t* o1, int64_t os, const int32_t* slot,
                   const uint32_t* a0, const uint32_t* a1, int64_t as, const uint32_t* b0,
                   const uint32_t* b1, int64_t bs, int64_t B, cudaStream_t st) {
-  if constexpr (LOGN >= 13 && LOGN <= 14) {
-    if (c->ks_tmem) {
-      auto kt = c->ks_tmem == 2 ? k_keyswitch_tm<LOGN, 5, true> : k_keyswitch_tm<LOGN, 4, false>;
-      const int nthreads = c->ks_tmem == 2 ? Geo<LOGN, 5>::NT : Geo<LOGN, 4>::NT;
-      const size_t sm = ks_tm_smem<LOGN>();
-      HEFV_CUDA(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      const int64_t chunk = 65535ll * KS_CTS_PER_CTA;
-      for (int64_t b0i = 0; b0i < B; b0i += chunk) {
-        const int64_t nb = (B - b0i) < chunk ? (B - b0i) : chunk;
-        dim3 grid(c->k, (unsigned)((nb + KS_CTS_PER_CTA - 1) / KS_CTS_PER_CTA));
-        kt<<<grid, nthreads, sm, st>>>(
-            kb, km, dig + b0i * ds, ds, o0, o1, os, slot ? slot + b0i : nullptr,
-            a0 ? a0 + b0i * as : nullptr, a1 ? a1 + b0i * as : nullptr, as, b0, b1, bs, nb,
-            c->k, c->d_tw32, c->d_itw32, c->d_info32);
-        HEFV_LAUNCH_CHECK("k_keyswitch_tm");
-        if (!slot && nb < B) {
-          o0 += nb * os;
-          o1 += nb * os;
-          if (b0) b0 += nb * bs;
-          if (b1) b1 += nb * bs;
-        }
-      }
-      return 0;
-    }
-  }
-  if constexpr (LOGN == 14) {
-    if (c->ks_e32) return run_ks_plain<14, 5>(c, kb, km, dig, ds, o0, o1, os, slot, a0, a1, as, b0,
-                                              b1, bs, B, st);
-  }
   return run_ks_plain<LOGN, KsLoge<LOGN>::v>(c, kb, km, dig, ds, o0, o1, os, slot, a0, a1, as, b0,
                                              b1, bs, B, st);
 }
@@ -410,7 +174,7 @@ static int run_ks_plain(hefv_ctx* c, const uint32_t* kb, const uint32_t* km, con
                         const uint32_t* a0, const uint32_t* a1, int64_t as, const uint32_t* b0,
                         const uint32_t* b1, int64_t bs, int64_t B, cudaStream_t st) {
   typedef Geo<LOGN, LE> G_;
-  auto kern = (c->ks_prefetch && LOGN >= 10) ? k_keyswitch<LOGN, LE, true> : k_keyswitch<LOGN, LE, false>;
+  auto kern = k_keyswitch<LOGN, LE>;
   const size_t smem = (size_t)(1 << (LOGN - G_::RLAST)) * sizeof(uint2) +
                       ((size_t)G_::N + (size_t)((spad_size(G_::N) + 3) & ~3)) * 4 + 16;
   if (smem > 48 * 1024) {

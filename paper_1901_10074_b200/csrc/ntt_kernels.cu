@@ -8,15 +8,12 @@
 //   * k_ntt_cl_fwd / k_ntt_cl_inv: polynomials larger than one SM (64-bit
 //     N = 2^15 / 2^16, 30-bit N = 2^16) as one thread-block cluster each,
 //     the CTA-spanning exchange through distributed shared memory;
-//   * k_ntt64_radix_pass: the four-pass global-memory fallback for 64-bit
-//     2^15 / 2^16 (HEFV_NTT64_CLUSTER=0).
 #include <cstdlib>
 
 #include "../../include/hefv.h"
 #include "internal.h"
 #include "ntt.cuh"
 #include "kcommon.cuh"
-#include "tmem.cuh"
 #include "cluster.cuh"
 
 namespace hefv {
@@ -356,18 +353,12 @@ static int launch_b32(bool fwd, const uint32_t* in, uint32_t* out, int64_t batch
 }
 
 // 64-bit device-order transform variant: 0 = one CTA per polynomial
-// (k_ntt_fwd/inv), 1 = persistent with twiddles from L1/L2, 2 = persistent
-// with staged twiddles.  Default = the measured best per (N, direction) on a
-// B200 (60-bit primes, L = 8, batch 256-1024): persistent for 2^13 and the
-// 2^14 inverse (0.62-0.67 of the butterfly peak vs 0.57-0.61), one CTA per
-// polynomial elsewhere (staging never won).  HEFV_NTT64_B overrides.
+// (k_ntt_fwd/inv), 1 = persistent with twiddles from L1/L2.  The measured
+// best per (N, direction) on a B200 (60-bit primes, L = 8, batch 256-1024):
+// persistent for 2^13 and the 2^14 inverse (0.62-0.67 of the butterfly peak
+// vs 0.57-0.61), one CTA per polynomial elsewhere.  (Staging the twiddles in
+// shared memory never won and is not built.)
 static int ntt64_mode(int log_n, bool fwd) {
-  static int env = -2;
-  if (env == -2) {
-    const char* v = std::getenv("HEFV_NTT64_B");
-    env = v ? std::atoi(v) : -1;
-  }
-  if (env >= 0) return env;
   return (log_n == 13 || (log_n == 14 && !fwd)) ? 1 : 0;
 }
 
@@ -377,8 +368,7 @@ static int launch_b64(bool fwd, const uint64_t* in, uint64_t* out, int64_t batch
                       bool stage, int bcast) {
   typedef Geo<LOGN, 4> G_;
   const size_t smem = Ntt64B<LOGN>::smem(stage);
-  auto kern = fwd ? (stage ? k_ntt64_b<LOGN, true, true> : k_ntt64_b<LOGN, true, false>)
-                  : (stage ? k_ntt64_b<LOGN, false, true> : k_ntt64_b<LOGN, false, false>);
+  auto kern = fwd ? k_ntt64_b<LOGN, true, false> : k_ntt64_b<LOGN, false, false>;
   HEFV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 1;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G_::NT, smem) != cudaSuccess ||
@@ -415,7 +405,7 @@ static int launch_one(bool fwd, const typename M::T* in, typename M::T* out, int
       return launch_b64<LOGN>(fwd, reinterpret_cast<const uint64_t*>(in),
                               reinterpret_cast<uint64_t*>(out), batch, nprimes, prime_base,
                               reinterpret_cast<const ulonglong2*>(tw),
-                              reinterpret_cast<const Prime64Info*>(info), st, mode == 2, bcast);
+                              reinterpret_cast<const Prime64Info*>(info), st, false, bcast);
   }
   if (total > 0x7fffffff) return fail("ntt: batch too large");
   if (fwd) {
@@ -478,6 +468,29 @@ int hefv_ntt64_large(hefv_ctx* c, bool fwd, const uint64_t* in, uint64_t* out, i
 int hefv_ntt32_large(hefv_ctx* c, bool fwd, const uint32_t* in, uint32_t* out, int64_t batch,
                      int nprimes, int prime_base, int natural, cudaStream_t st);
 
+// Pointwise products of canonical residues (NttPrime.negacyclic_mul's
+// middle step, ntt.py:226-227): element e of row (b, i) under prime
+// prime_base + i.
+__global__ void k_pointwise32(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
+                              uint32_t* __restrict__ out, int64_t total, int log_n, int nprimes,
+                              int prime_base, const Prime32Info* __restrict__ info) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)((e >> log_n) % nprimes);
+    const Prime32Info inf = info[prime_base + i];
+    out[e] = barrett62((uint64_t)a[e] * b[e], inf.p, inf.mu);
+  }
+}
+__global__ void k_pointwise64(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
+                              uint64_t* __restrict__ out, int64_t total, int log_n, int nprimes,
+                              int prime_base, const Prime64Info* __restrict__ info) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)((e >> log_n) % nprimes);
+    out[e] = mulmod64(a[e], b[e], info[prime_base + i].p);
+  }
+}
+
 extern "C" {
 
 int hefv_ntt_fwd32(hefv_ctx* c, const uint32_t* in, uint32_t* out, int64_t batch,
@@ -530,6 +543,27 @@ int hefv_ntt_inv64(hefv_ctx* c, const uint64_t* in, uint64_t* out, int64_t batch
   return r;
 }
 
+int hefv_pointwise_mul(hefv_ctx* c, int32_t wide, const void* a, const void* b, void* out,
+                       int64_t batch, int32_t nprimes, int32_t prime_base, void* stream) {
+  if (!c) return fail("pointwise_mul: null context");
+  const int nset = wide ? c->n64 : c->n32;
+  if (nprimes < 1 || prime_base < 0 || prime_base + nprimes > nset)
+    return fail("pointwise_mul: prime range outside the context");
+  if (batch <= 0) return 0;
+  const int64_t total = batch * nprimes * (int64_t)c->n;
+  const unsigned grid = (unsigned)((total + 255) / 256 < 148 * 64 ? (total + 255) / 256 : 148 * 64);
+  if (wide)
+    k_pointwise64<<<grid, 256, 0, as_stream(stream)>>>(
+        static_cast<const uint64_t*>(a), static_cast<const uint64_t*>(b),
+        static_cast<uint64_t*>(out), total, c->log_n, nprimes, prime_base, c->d_info64);
+  else
+    k_pointwise32<<<grid, 256, 0, as_stream(stream)>>>(
+        static_cast<const uint32_t*>(a), static_cast<const uint32_t*>(b),
+        static_cast<uint32_t*>(out), total, c->log_n, nprimes, prime_base, c->d_info32);
+  HEFV_LAUNCH_CHECK("k_pointwise");
+  return 0;
+}
+
 }  // extern "C"
 
 // Forward transforms (device order) of `rows` input rows under every 64-bit
@@ -553,81 +587,6 @@ int hefv_ntt64_fwd_rows(hefv_ctx* c, const uint64_t* in, uint64_t* out, int64_t 
 // the single-CTA transform, so results are identical.
 // ---------------------------------------------------------------------------
 namespace hefv {
-
-// Pass over stages [s0, s0 + R) of a length-N transform for blocks of 2^R
-// elements with element stride T = N >> (s0 + R).  One thread per block.
-template <int R, bool FWD>
-__global__ void __launch_bounds__(256)
-    k_ntt64_radix_pass(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, int log_n,
-                       int s0, int nprimes, int prime_base, int64_t nblocks_per_poly,
-                       int64_t total_blocks, const ulonglong2* __restrict__ tw_all,
-                       const Prime64Info* __restrict__ info, int last_inverse, int canon_out) {
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= total_blocks) return;
-  const int64_t poly = gid / nblocks_per_poly;
-  const int64_t blk = gid % nblocks_per_poly;
-  const int n = 1 << log_n;
-  const int pi = prime_base + (int)(poly % nprimes);
-  const Prime64Info inf = info[pi];
-  const Mod64 md{inf.p, 2 * inf.p};
-  const ulonglong2* tw = tw_all + (size_t)pi * n;
-  const int tsh = log_n - s0 - R;
-  const int64_t L = blk & ((1ll << tsh) - 1);
-  const int64_t G = blk >> tsh;
-  const int64_t base = (G << (log_n - s0)) + L;
-  const uint64_t* src = in + poly * n;
-  uint64_t* dst = out + poly * n;
-  uint64_t x[1 << R];
-#pragma unroll
-  for (int e = 0; e < (1 << R); ++e) x[e] = src[base + ((int64_t)e << tsh)];
-  if (FWD) {
-    if (s0 == 0) {
-#pragma unroll
-      for (int e = 0; e < (1 << R); ++e) x[e] = reduce_any(x[e], inf);
-    }
-#pragma unroll
-    for (int l = 0; l < R; ++l) {
-      const int half = (1 << R) >> (l + 1);
-      const ulonglong2* twb = tw + (1ll << (s0 + l)) + (G << l);
-#pragma unroll
-      for (int u = 0; u < (1 << l); ++u) {
-        const ulonglong2 w = twb[u];
-#pragma unroll
-        for (int e0 = 0; e0 < half; ++e0) {
-          const int e = u * 2 * half + e0;
-          md.ct(x[e], x[e + half], w);
-        }
-      }
-    }
-    if (canon_out) {
-#pragma unroll
-      for (int e = 0; e < (1 << R); ++e) x[e] = md.canon4(x[e]);
-    }
-  } else {
-#pragma unroll
-    for (int l = R - 1; l >= 0; --l) {
-      const int half = (1 << R) >> (l + 1);
-      const ulonglong2* twb = tw + (1ll << (s0 + l)) + (G << l);
-#pragma unroll
-      for (int u = 0; u < (1 << l); ++u) {
-#pragma unroll
-        for (int e0 = 0; e0 < half; ++e0) {
-          const int e = u * 2 * half + e0;
-          if (last_inverse && s0 + l == 0)
-            md.gs_last(x[e], x[e + half], inf.ninv, inf.wn);
-          else
-            md.gs(x[e], x[e + half], twb[u]);
-        }
-      }
-    }
-    if (canon_out) {
-#pragma unroll
-      for (int e = 0; e < (1 << R); ++e) x[e] = md.subp(x[e]);
-    }
-  }
-#pragma unroll
-  for (int e = 0; e < (1 << R); ++e) dst[base + ((int64_t)e << tsh)] = x[e];
-}
 
 __global__ void k_permute_bitrev64(const uint64_t* __restrict__ in, uint64_t* __restrict__ out,
                                    int log_n, int64_t total) {
@@ -832,15 +791,6 @@ static int launch_cl64(bool fwd, const uint64_t* in, uint64_t* out, int64_t tota
                                           st, bcast);
 }
 
-static bool ntt64_cluster_enabled() {
-  static int m = -1;
-  if (m < 0) {
-    const char* v = std::getenv("HEFV_NTT64_CLUSTER");
-    m = v ? std::atoi(v) : 1;
-  }
-  return m != 0;
-}
-
 }  // namespace hefv
 
 int hefv_ntt64_large(hefv_ctx* c, bool fwd, const uint64_t* in, uint64_t* out, int64_t batch,
@@ -849,9 +799,9 @@ int hefv_ntt64_large(hefv_ctx* c, bool fwd, const uint64_t* in, uint64_t* out, i
   const int64_t n = c->n;
   const int64_t total_polys = batch * nprimes;
   if (total_polys <= 0) return 0;
-  if (bcast && !((log_n == 15 || log_n == 16) && ntt64_cluster_enabled()))
+  if (bcast && !(log_n == 15 || log_n == 16))
     return fail("ntt64: broadcast input rows need the cluster transform");
-  if ((log_n == 15 || log_n == 16) && ntt64_cluster_enabled()) {
+  if (log_n == 15 || log_n == 16) {
     auto run = [&](const uint64_t* a, uint64_t* b) {
       const ulonglong2* tw = fwd ? c->d_tw64 : c->d_itw64;
       return log_n == 15
@@ -881,73 +831,7 @@ int hefv_ntt64_large(hefv_ctx* c, bool fwd, const uint64_t* in, uint64_t* out, i
     HEFV_LAUNCH_CHECK("ntt64 permute");
     return run(out, out);
   }
-  // radix-16 passes: stages in groups of 4 (log_n = 15 -> 4,4,4,3; 16 -> 4,4,4,4)
-  const int64_t blocks16 = n / 16;
-  const int threads = 256;
-  auto grid_for = [&](int64_t nb) { return (unsigned)((nb * total_polys + threads - 1) / threads); };
-  // the transform runs in place in `out`; the first pass reads `in`
-  const uint64_t* src = in;
-  if (fwd) {
-    int s0 = 0;
-    while (s0 < log_n) {
-      const int r = (log_n - s0) >= 4 ? 4 : (log_n - s0);
-      const bool last = s0 + r == log_n;
-      const int64_t nb = n >> r;
-      if (r == 4)
-        k_ntt64_radix_pass<4, true><<<grid_for(nb), threads, 0, st>>>(
-            src, out, log_n, s0, nprimes, prime_base, nb, nb * total_polys, c->d_tw64, c->d_info64,
-            0, last ? 1 : 0);
-      else
-        k_ntt64_radix_pass<3, true><<<grid_for(nb), threads, 0, st>>>(
-            src, out, log_n, s0, nprimes, prime_base, nb, nb * total_polys, c->d_tw64, c->d_info64,
-            0, last ? 1 : 0);
-      HEFV_LAUNCH_CHECK("ntt64 large pass");
-      src = out;
-      s0 += r;
-    }
-    if (natural) {
-      // out holds device order; permute into a temporary then copy back
-      uint64_t* tmp = nullptr;
-      HEFV_CUDA(cudaMallocAsync(&tmp, total_polys * n * 8, st));
-      const int64_t tot = total_polys * n;
-      k_permute_bitrev64<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(out, tmp, log_n, tot);
-      HEFV_LAUNCH_CHECK("ntt64 permute");
-      HEFV_CUDA(cudaMemcpyAsync(out, tmp, tot * 8, cudaMemcpyDeviceToDevice, st));
-      HEFV_CUDA(cudaFreeAsync(tmp, st));
-    }
-  } else {
-    if (natural) {
-      const int64_t tot = total_polys * n;
-      k_permute_bitrev64<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(in, out, log_n, tot);
-      HEFV_LAUNCH_CHECK("ntt64 permute");
-      src = out;
-    }
-    // inverse: stages from log_n - 1 down to 0, passes in reverse grouping
-    std::vector<std::pair<int, int>> passes;  // (s0, r)
-    int s0 = 0;
-    while (s0 < log_n) {
-      const int r = (log_n - s0) >= 4 ? 4 : (log_n - s0);
-      passes.push_back({s0, r});
-      s0 += r;
-    }
-    for (int pi = (int)passes.size() - 1; pi >= 0; --pi) {
-      const int ps = passes[pi].first, r = passes[pi].second;
-      const int64_t nb = n >> r;
-      const bool last = ps == 0;
-      if (r == 4)
-        k_ntt64_radix_pass<4, false><<<grid_for(nb), threads, 0, st>>>(
-            src, out, log_n, ps, nprimes, prime_base, nb, nb * total_polys, c->d_itw64,
-            c->d_info64, 1, last ? 1 : 0);
-      else
-        k_ntt64_radix_pass<3, false><<<grid_for(nb), threads, 0, st>>>(
-            src, out, log_n, ps, nprimes, prime_base, nb, nb * total_polys, c->d_itw64,
-            c->d_info64, 1, last ? 1 : 0);
-      HEFV_LAUNCH_CHECK("ntt64 large pass");
-      src = out;
-    }
-  }
-  (void)blocks16;
-  return 0;
+  return fail("ntt64_large: N must be 2^15 or 2^16");
 }
 
 // 32-bit primes at N = 2^16: the cluster transform (device order only).

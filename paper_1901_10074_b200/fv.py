@@ -95,6 +95,9 @@ class FvContext:
         self.pcol = np.array(self.q_primes, dtype=np.int64)[:, None]
         qc = CrtConstants.build(self.q_primes)
         self.q = qc.product
+        if self.q < 1 << 32:
+            # the exact t/q roundings run Knuth D on >= 2 words (hefv_fv_setup)
+            raise ParamMismatchError("the GPU backend needs q >= 2^32 (two or more q primes)")
         self.delta = self.q // fp.t
         self.delta_mod = [self.delta % p for p in self.q_primes]
         need_bits = n.bit_length() + 2 * self.q.bit_length() + 2
@@ -246,6 +249,14 @@ class FvContext:
                   out.data_ptr(), rows, br, cr, self.stream())
         return out
 
+    def mont_inv_rows(self):
+        """(1, k, N) stack holding 2^-32 mod p_j in row j (leaves Montgomery form)."""
+        if getattr(self, "_mont_inv", None) is None:
+            v = np.array([pow(1 << 32, -1, p) for p in self.q_primes], dtype=np.int64)
+            self._mont_inv = nat.to_device(
+                np.repeat(v[:, None], self.n, axis=1).astype(np.int32)[None])
+        return self._mont_inv
+
     def to_mont(self, a):
         out = _torch().empty_like(a)
         self.call("hefv_to_montgomery", a.data_ptr(), out.data_ptr(),
@@ -287,15 +298,18 @@ class SwitchKey:
                      self.aux_dev.data_ptr(), ctx.stream())
 
     def _host(self, dev):
-        """Device layout -> reference layout: undo Montgomery (x * 2^-32 mod p,
-        exact in u64 since x, 2^-32 mod p < 2^30) and the device NTT order."""
+        """Device layout -> reference layout: Montgomery form undone on the
+        device (x * (2^-32 mod p_j) mod p_j), then the device NTT order
+        permuted back to natural order on download."""
         ctx = self._ctx
-        host = nat.to_host(dev).astype(np.uint64)
+        # (j, i, N) -> (i, j, N): every digit row i is a stack over the primes j
+        t = dev.transpose(0, 1).contiguous()
+        plain = ctx.elementwise(2, t, ctx.mont_inv_rows(), b_rows=1).transpose(0, 1)
+        host = nat.to_host(plain.contiguous()).astype(np.int64)
         out = []
-        for j, p in enumerate(ctx.q_primes):
-            plain = (host[j] * np.uint64(pow(1 << 32, -1, p)) % np.uint64(p)).astype(np.int64)
-            nat_order = np.empty_like(plain)
-            nat_order[..., ctx.brev] = plain
+        for j in range(ctx.k):
+            nat_order = np.empty_like(host[j])
+            nat_order[..., ctx.brev] = host[j]
             out.append(nat_order)
         return out
 
@@ -303,16 +317,21 @@ class SwitchKey:
     def from_host(cls, ctx: FvContext, body, mask) -> "SwitchKey":
         """Upload a key in the reference's stored form (list over target prime
         j of (k, N) natural-order NTT values, fv.py:67-72) into the device
-        layout used by the key-switch kernel."""
+        layout used by the key-switch kernel: residues checked and permuted to
+        device order on the host, Montgomery form entered on the device."""
 
         def dev(stacks):
             if len(stacks) != ctx.k or any(np.shape(s) != (ctx.k, ctx.n) for s in stacks):
                 raise FormatError("switch key does not match the parameter set")
-            arr = np.empty((ctx.k, ctx.k, ctx.n), dtype=np.uint32)
+            arr = np.empty((ctx.k, ctx.k, ctx.n), dtype=np.int64)
             for j, p in enumerate(ctx.q_primes):
-                x = ctx.natural_to_dev(np.asarray(stacks[j], dtype=np.int64)).astype(np.uint64)
-                arr[j] = ((x % np.uint64(p)) << np.uint64(32)) % np.uint64(p)
-            return nat.to_device(arr.view(np.int32))
+                x = ctx.natural_to_dev(np.asarray(stacks[j], dtype=np.int64))
+                if (x < 0).any() or (x >= p).any():
+                    raise FormatError("switch key residue outside [0, p_j)")
+                arr[j] = x
+            d = nat.to_device(arr.astype(np.int32))            # (j, i, N)
+            t = d.transpose(0, 1).contiguous()                   # (i, j, N)
+            return ctx.to_mont(t).transpose(0, 1).contiguous()   # back to (j, i, N)
 
         return cls(ctx, dev(body), dev(mask))
 

@@ -63,7 +63,7 @@ class NttPrime:
             nat._lib.hefv_ctx_destroy(h)
             self._h = None
 
-    def _run(self, a, forward: bool) -> np.ndarray:
+    def _upload(self, a):
         torch = self._torch
         arr = np.asarray(a)
         if arr.shape[-1] != self.n:
@@ -75,21 +75,29 @@ class NttPrime:
             flat = np.array([[int(v) % self.p for v in row] for row in flat], dtype=np.uint64)
         else:
             flat = np.mod(flat.astype(np.int64), self.p).astype(np.uint64)
-        batch = flat.shape[0]
-        stream = nat.stream_handle()
         if self.wide:
             dev = torch.from_numpy(flat.view(np.int64)).cuda()
-            out = torch.empty_like(dev)
-            fn = "hefv_ntt_fwd64" if forward else "hefv_ntt_inv64"
         else:
             dev = torch.from_numpy(flat.astype(np.int32)).cuda()
-            out = torch.empty_like(dev)
+        return dev, lead
+
+    def _transform(self, dev, forward: bool):
+        out = self._torch.empty_like(dev)
+        if self.wide:
+            fn = "hefv_ntt_fwd64" if forward else "hefv_ntt_inv64"
+        else:
             fn = "hefv_ntt_fwd32" if forward else "hefv_ntt_inv32"
-        nat.call(fn, self._h, dev.data_ptr(), out.data_ptr(), batch, 1, 0, 1, stream)
-        res = out.cpu().numpy().astype(np.int64).reshape(*lead, self.n)
-        if self.dtype is object:
-            res = res.astype(object)
-        return res
+        nat.call(fn, self._h, dev.data_ptr(), out.data_ptr(), dev.shape[0], 1, 0, 1,
+                 nat.stream_handle())
+        return out
+
+    def _download(self, dev, lead) -> np.ndarray:
+        res = dev.cpu().numpy().astype(np.int64).reshape(*lead, self.n)
+        return res.astype(object) if self.dtype is object else res
+
+    def _run(self, a, forward: bool) -> np.ndarray:
+        dev, lead = self._upload(a)
+        return self._download(self._transform(dev, forward), lead)
 
     def fwd(self, a) -> np.ndarray:
         """Evaluations at the odd powers of psi, natural order (ntt.py:216-219)."""
@@ -100,11 +108,18 @@ class NttPrime:
         return self._run(ev, False)
 
     def negacyclic_mul(self, a, b) -> np.ndarray:
-        fa = self.fwd(a)
-        fb = self.fwd(b)
-        prod = (fa.astype(object) * fb.astype(object)) % self.p
-        return self.inv(np.asarray(prod, dtype=np.uint64).astype(np.int64) if self.p < _U64_LIMIT
-                        else prod)
+        """Ring product mod (x^N + 1, p) (ntt.py:226-227): both transforms,
+        the pointwise product and the inverse on the device."""
+        da, lead = self._upload(a)
+        db, lead_b = self._upload(b)
+        if lead != lead_b:
+            raise ValueError("operands must have the same shape")
+        fa = self._transform(da, True)
+        fb = self._transform(db, True)
+        prod = self._torch.empty_like(fa)
+        nat.call("hefv_pointwise_mul", self._h, 1 if self.wide else 0, fa.data_ptr(),
+                 fb.data_ptr(), prod.data_ptr(), fa.shape[0], 1, 0, nat.stream_handle())
+        return self._download(self._transform(prod, False), lead)
 
 
 class CrtBasis:

@@ -96,3 +96,41 @@ def test_keyswitch64_large_n_matches_oracle():
     got = ks.switch_host(ks.upload_key(body, mask), c[None], "aux")
     assert np.array_equal(got[0, 0].astype(object), np.asarray(d0, dtype=object))
     assert np.array_equal(got[0, 1].astype(object), np.asarray(d1, dtype=object))
+
+
+_KS64 = None
+
+
+def _ks64_gold():
+    global _KS64
+    if _KS64 is None:
+        import json
+        from pathlib import Path
+
+        _KS64 = json.loads((Path(__file__).resolve().parent / "golden" / "ks64.json")
+                           .read_text())["cases"]
+    return _KS64
+
+
+@pytest.mark.parametrize("case", [pytest.param(i, marks=pytest.mark.slow) if i >= 5 else i
+                                  for i in range(7)])
+def test_keyswitch64_matches_reference_golden(case):
+    """Config 4 pinned to the REFERENCE: _keyswitch_key + _keyswitch_apply
+    (fv.py:176-217) over _FvContext(FvParams(N, t, 60-bit primes)) ran in
+    tests/golden/make_golden.py --ks64 for (N, L) in {2^12, 2^14} x {2, 4, 8}
+    and (2^16, 2).  The oracle regenerates the same key and input from the
+    seed (their digests must equal the reference's), and both GPU paths
+    (direct 64-bit and aux basis) must return the reference's d0 / d1."""
+    from paper_1901_10074_b200.rns import RnsKeySwitch64
+
+    g = _ks64_gold()[case]
+    n, primes = g["n"], g["primes"]
+    key, c = O.ks64_case(primes, n, g["seed"])
+    assert O.limb_digest(list(key.body) + list(key.mask)) == g["key"]
+    assert O.limb_digest([c]) == g["c"]
+    ks = RnsKeySwitch64(primes, n, aux=True)
+    dev_key = ks.upload_key(key.body, key.mask)
+    for path in ("direct", "aux"):
+        got = ks.switch_host(dev_key, c.astype(object)[None], path)
+        assert O.limb_digest([got[0, 0].astype(np.int64)]) == g["d0"], path
+        assert O.limb_digest([got[0, 1].astype(np.int64)]) == g["d1"], path
