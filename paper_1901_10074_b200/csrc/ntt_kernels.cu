@@ -114,10 +114,25 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT)
 // 2^14) also live in shared memory, as single-word Montgomery forms (the
 // Shoup pairs would not fit next to the tile and the stage); the last pass
 // then uses Montgomery products instead of L2-latency-bound Shoup loads.
+// N with the last pass's twiddles in shared memory (2^12: inverse 0.60 ->
+// 0.63 of the butterfly peak, forward unchanged; measured on a B200)
+#ifndef NTT32_LASTSM_MASK
+#define NTT32_LASTSM_MASK ((1 << 14) | (1 << 12))
+#endif
+#ifndef NTT32_MINB_SMALL
+#define NTT32_MINB_SMALL 0  // 0: 1024 / NT resident CTAs per SM for N <= 2^12
+#endif
+template <int LOGN>
+constexpr int ntt32_minb() {
+  return (Geo<LOGN, 4>::NT <= 256 && NTT32_MINB_SMALL) ? NTT32_MINB_SMALL
+                                                       : 1024 / Geo<LOGN, 4>::NT;
+}
+
 template <int LOGN, bool FWD>
 struct Ntt32B {
   typedef Geo<LOGN, 4> G_;
-  static constexpr bool LASTSM = LOGN == 14;  // fwd: last pass; inv: its first pass
+  // fwd: last pass; inv: its first pass
+  static constexpr bool LASTSM = ((NTT32_LASTSM_MASK >> LOGN) & 1) != 0;
   static constexpr int NTW = 1 << (LOGN - G_::RLAST);
   static constexpr size_t smem = (size_t)NTW * sizeof(uint2) +
                                  (size_t)((spad_size(G_::N) + 3) & ~3) * 4 + (size_t)G_::N * 4 +
@@ -125,7 +140,7 @@ struct Ntt32B {
 };
 
 template <int LOGN, bool FWD>
-__global__ void __launch_bounds__(Geo<LOGN, 4>::NT, 1024 / Geo<LOGN, 4>::NT)
+__global__ void __launch_bounds__(Geo<LOGN, 4>::NT, ntt32_minb<LOGN>())
     k_ntt32_b(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int64_t batch,
               int nprimes, int prime_base, const uint2* __restrict__ tw_all,
               const Prime32Info* __restrict__ info, const uint32_t* __restrict__ twm_all) {

@@ -359,7 +359,9 @@ def _tile_rows(backend, n_plain_per_row: float) -> int:
     ctx = backend.ctx
     ct_bytes = 2 * ctx.k * ctx.n * 4
     per_row = 2 * ct_bytes + n_plain_per_row * (ctx.k * ctx.n * 4 + ctx.n * 8)
-    return int(max(1, min(8192, _budget(_TILE_BYTES) // per_row)))
+    # a tile's (T, 2, k, N) word count stays below 2^31 (32-bit element indices)
+    words_cap = ((1 << 31) - 1) // (2 * ctx.k * ctx.n)
+    return int(max(1, min(8192, words_cap, _budget(_TILE_BYTES) // per_row)))
 
 
 def _run_rows(backend, rows, x, seg_lists, active, m_arr, off_arr, bias_arr, out_dev, n_iter,
