@@ -11,6 +11,8 @@
 //   kind 6: mad.wide.u32 into a 64-bit running sum whose bits feed the next
 //           multiplier (a dependent chain: the product cannot be hoisted)
 //   kind 7: DFMA (fp64 fused multiply-add)
+//   kind 8: the kind-4 butterfly with its quotient on the FP64 pipe
+//   kind 9: kinds 4 and 8 interleaved (half the chains each)
 // Each thread runs 8 independent chains so the pipes, not latency, bound it.
 #include "../../include/hefv.h"
 #include "internal.h"
@@ -68,6 +70,18 @@ __global__ void __launch_bounds__(256) k_probe(uint32_t* out, int iters, uint32_
           a[i] = (uint32_t)t ^ (uint32_t)(t >> 32);
         } else if (KIND == 3) {
           a[i] = a[i] + b[i] + 0x777u;
+        } else if (KIND == 8 || (KIND == 9 && (i & 1))) {
+          // the same butterfly with the Shoup quotient taken on the FP64
+          // pipe: q = rint(y * w / p) from y as an exact double (magic-
+          // number conversion), t = y w - q p + p in [0, 2p)
+          const uint32_t w = 123456789u;
+          const double wf = 123456789.0 / 1073692673.0;
+          uint32_t x = min(a[i], a[i] - p2);
+          const double yd = __hiloint2double(0x43300000, b[i]) - 4503599627370496.0;
+          const uint32_t q = (uint32_t)__double2loint(fma(yd, wf, 6755399441055744.0));
+          const uint32_t t = b[i] * w + p - q * p;
+          a[i] = x + t;
+          b[i] = x - t + p2;
         } else {
           // x = a[i], y = b[i] butterfly with twiddle (w, wsh)
           const uint32_t w = 123456789u, wsh = 493903u;
@@ -166,6 +180,12 @@ extern "C" int hefv_probe_int(int32_t kind, int32_t blocks, int32_t iters, uint3
       break;
     case 7:
       k_probe_dfma<<<blocks, 256, 0, st>>>(out, iters, 7u);
+      break;
+    case 8:
+      k_probe<8><<<blocks, 256, 0, st>>>(out, iters, 7u);
+      break;
+    case 9:
+      k_probe<9><<<blocks, 256, 0, st>>>(out, iters, 7u);
       break;
     default:
       return fail("hefv_probe_int: unknown kind");

@@ -26,6 +26,6 @@ def measure(kind, blocks=148 * 8, iters=2000):
 
 if __name__ == "__main__":
     names = ["imad", "imad_hi", "imad_wide", "iadd3", "shoup_butterfly", "shoup_butterfly64",
-             "mad_wide_acc", "dfma"]
+             "mad_wide_acc", "dfma", "butterfly_fp64q", "butterfly_mixed"]
     res = {n: measure(k) / 1e12 for k, n in enumerate(names)}
     print(json.dumps({"unit": "Tops/s", **{k: round(v, 3) for k, v in res.items()}}))
