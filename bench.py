@@ -190,9 +190,8 @@ def run_ours(args, rank, local_rank, world):
     _barrier(world)
 
     # ---- timed region: device-resident step, KS launches bracketed by events
-    planner.KS_EVENTS = []
+    planner.ks_reset(be.ctx, timing=True)
     launches0 = nat.launch_count()
-    ks0 = dict(planner.STATS)
     clocks = ClockSampler(local_rank)
     clocks.start()
     torch.cuda.synchronize()
@@ -208,12 +207,9 @@ def run_ours(args, rank, local_rank, world):
     clk = clocks.stop()
     step_ms = e0.elapsed_time(e1) / args.steps
     launches = (nat.launch_count() - launches0) / args.steps
-    ks_events = planner.KS_EVENTS
-    planner.KS_EVENTS = None
-    ks_ms = sum(a.elapsed_time(b) for a, b, _ in ks_events)
-    ks_cts = sum(bt for _, _, bt in ks_events)
-    ks_launches = len(ks_events)
-    del ks0
+    ks = planner.ks_stats(be.ctx)
+    planner.ks_reset(be.ctx)
+    ks_ms, ks_cts, ks_launches = ks["ks_ms"], ks["ks_cts"], ks["ks_launches"]
     step_ms = _max_over_ranks(step_ms, world)
 
     # ---- e2e through the public API with host buffers
@@ -396,7 +392,7 @@ def _config3_leg():
     be = FvBackend(params, rng=np.random.default_rng(KEY_SEED))
     torch.cuda.synchronize()
     keygen_s = time.perf_counter() - t0
-    planner.STATS.update(ks_launches=0, ks_cts=0)
+    planner.ks_reset(be.ctx)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     wall = time.perf_counter()
     e0.record()
@@ -406,11 +402,12 @@ def _config3_leg():
     wall = time.perf_counter() - wall
     ms = e0.elapsed_time(e1)
     want = centred_mod(plaintext_forward(net, img), params.plain_modulus)
+    ks = planner.ks_stats(be.ctx)
     planner.release_workspace(be.ctx)
     torch.cuda.empty_cache()
     return {"ms": round(ms, 1), "wall_s": round(wall, 2), "keygen_s": round(keygen_s, 2),
             "q_primes": be.ctx.k, "logits_exact": [int(v) for v in logits] == want,
-            "ks_launches": planner.STATS["ks_launches"], "ks_cts": planner.STATS["ks_cts"],
+            "ks_launches": ks["ks_launches"], "ks_cts": ks["ks_cts"],
             "serial_op_counts": workload_op_counts(3),
             "path": "pack_image(host pixels) + infer + decrypt_logits(host logits), 1 image"}, be
 

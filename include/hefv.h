@@ -265,6 +265,105 @@ int hefv_ks64_aux_key(hefv_ctx* ctx, const uint64_t* kbody, const uint64_t* kmas
 int hefv_keyswitch64_aux(hefv_ctx* ctx, const uint32_t* kaux, const uint64_t* digits,
                          uint64_t* out, uint32_t* scratch, int64_t B, void* stream);
 
+/* ---- object-level surface ---------------------------------
+ * What a host without torch needs to run the reference's FvBackend ops
+ * (fv.py:254-432) on the device.  Ciphertexts are device buffers of
+ * (nparts, k, N) uint32 residues; host buffers use the reference's int64
+ * (nparts, k, N) layout (FvCiphertext.parts, fv.py:30-42; serialize.py:80-85).
+ * Switch keys are opaque handles.  Plaintext slot vectors are DEVICE
+ * (N/2) uint64 arrays of residues mod t (engine.py:138-153 pads them).
+ * Temporaries are stream-ordered (cudaMallocAsync on `stream`); unless noted,
+ * `out` may alias an input. */
+typedef struct hefv_key hefv_key;
+
+/* cudaMalloc / cudaFree of one (nparts, k, N) ciphertext buffer. */
+int hefv_ct_alloc(hefv_ctx* ctx, int32_t nparts, uint32_t** out);
+int hefv_ct_free(hefv_ctx* ctx, uint32_t* ct);
+/* Host int64 (nparts, k, N) <-> device; upload rejects residues outside
+ * [0, p_j) (the reference reads them with `% p`, fv.py:30-42). Synchronous. */
+int hefv_ct_upload(hefv_ctx* ctx, const int64_t* host, int32_t nparts, uint32_t* ct,
+                   void* stream);
+int hefv_ct_download(hefv_ctx* ctx, const uint32_t* ct, int32_t nparts, int64_t* host,
+                     void* stream);
+
+/* Switch key (fv.py:67-72, _keyswitch_key fv.py:176-202) in the reference's
+ * stored form: body/mask (k, k, N) int64 = [target prime j][digit i][natural
+ * NTT order], as serialize.read_keyset returns it.  Checked, permuted to
+ * device order and Montgomery form on the device, and (when the context has
+ * hefv_ks_aux_setup) converted to the aux-basis form.  Synchronous. */
+int hefv_key_upload(hefv_ctx* ctx, const int64_t* body, const int64_t* mask, hefv_key** out,
+                    void* stream);
+/* Handle over device-resident key material already in the device layout
+ * (hefv_keygen_digit output; aux form from hefv_ks_aux_key, required when
+ * the context uses the aux key switch).  Does not take ownership. */
+int hefv_key_wrap(hefv_ctx* ctx, const uint32_t* body, const uint32_t* mask, const uint32_t* aux,
+                  hefv_key** out);
+int hefv_key_free(hefv_key* key);
+
+/* _encrypt (fv.py:317-335) of B slot vectors (B, N/2): encode, Delta m, then
+ * hefv_encrypt with the host-drawn u, e1, e2 (B, N).  out (B, 2, k, N). */
+int hefv_encrypt_slots(hefv_ctx* ctx, const uint32_t* pk_ntt, const int8_t* u, const int8_t* e1,
+                       const int8_t* e2, const uint64_t* slots, uint32_t* out, int64_t B,
+                       void* stream);
+/* _decrypt (fv.py:337-353): B ciphertexts of nparts parts -> (B, N/2) slots. */
+int hefv_decrypt_slots(hefv_ctx* ctx, const uint32_t* ct, int32_t nparts, const uint32_t* s_ntt,
+                       const uint32_t* s2_ntt, uint64_t* slots, int64_t B, void* stream);
+/* _add (fv.py:355-357): limb-wise sum of nparts parts. */
+int hefv_add(hefv_ctx* ctx, const uint32_t* a, const uint32_t* b, int32_t nparts, uint32_t* out,
+             void* stream);
+/* _add_plain (fv.py:359-362): c0 + Delta * encode(slots), other parts copied. */
+int hefv_add_plain(hefv_ctx* ctx, const uint32_t* ct, int32_t nparts, const uint64_t* slots,
+                   uint32_t* out, void* stream);
+/* _cmult (fv.py:364-375): every part times centred(encode(slots)). */
+int hefv_cmult(hefv_ctx* ctx, const uint32_t* ct, int32_t nparts, const uint64_t* slots,
+               uint32_t* out, void* stream);
+/* One rotation hop of _rotate (fv.py:417-432): out = (sigma_g(c0), 0) +
+ * KS_key(sigma_g(c1)), g = 3^offset mod 2N and `key` the Galois key of that
+ * offset.  A rotation by an offset without its own key is the ascending
+ * power-of-two hops (fv.py:422-425), one call each. */
+int hefv_rotate(hefv_ctx* ctx, const uint32_t* ct, uint32_t galois_elt, const hefv_key* key,
+                uint32_t* out, void* stream);
+/* _mult + _relinearize (fv.py:377-415): exact BFV tensor of two 2-part
+ * ciphertexts (b may equal a) and the relinearisation key switch. */
+int hefv_mult(hefv_ctx* ctx, const uint32_t* a, const uint32_t* b, const hefv_key* relin,
+              uint32_t* out, void* stream);
+
+/* ---- batched layer rows (the planner; inference.py:261-349) --------------
+ * x: (x_cts, 2, k, N) layer input ciphertexts.  R rows, grouped by output
+ * ciphertext (row_out ascending); row r: output ciphertext row_out[r] < nout,
+ * slot offset row_off[r] (= out_index % s; its piece is rotated by -off),
+ * bias row_bias[r] mod t (0 = none; row_bias may be NULL), plaintexts
+ * [row_ptr[r], row_ptr[r+1]) -- plaintext p multiplies input ciphertext
+ * plain_seg[p] and has entries [plain_ptr[p], plain_ptr[p+1]) of (slot
+ * slot_idx[e] < N/2, value slot_val[e] < t).  AllSum has n_iter steps
+ * (shift 2^j); Galois keys by rotation offset (key_offsets[i] -> keys[i])
+ * must include every power of two below 2^n_iter and every placement hop.
+ * The pieces are ADDED into out (nout, 2, k, N).  All plan arrays are host
+ * memory; work: device words >= hefv_layer_rows_work_words(...);
+ * ks_scratch: ks_cts * 9 k N words (aux key switch; may be NULL otherwise).
+ * Same limbs as the reference's per-row loop. */
+int hefv_layer_rows_work_words(hefv_ctx* ctx, int32_t x_cts, int64_t R, const int64_t* row_ptr,
+                               int64_t tile_rows, int64_t* words);
+int hefv_layer_rows(hefv_ctx* ctx, const uint32_t* x, int32_t x_cts, int64_t R,
+                    const int32_t* row_out, const int32_t* row_off, const uint64_t* row_bias,
+                    const int64_t* row_ptr, const int32_t* plain_seg, const int64_t* plain_ptr,
+                    const int32_t* slot_idx, const uint64_t* slot_val, int32_t n_iter,
+                    int32_t slot_count, int32_t nkeys, const int32_t* key_offsets,
+                    hefv_key* const* keys, uint32_t* out, int32_t nout, int64_t tile_rows,
+                    uint32_t* work, int64_t work_words, uint32_t* ks_scratch, int64_t ks_cts,
+                    void* stream);
+
+/* ---- key-switch accounting --------------------------------------------------
+ * Every hefv_keyswitch / hefv_keyswitch_aux call (direct or from the ops
+ * above) is counted; with timing enabled a CUDA event pair brackets it on
+ * its stream.  hefv_ks_timing resets; hefv_ks_stats synchronises on the
+ * recorded events and returns calls, ciphertexts and the summed ms. */
+int hefv_ks_timing(hefv_ctx* ctx, int32_t enable);
+int hefv_ks_stats(hefv_ctx* ctx, int64_t* calls, int64_t* cts, double* ms);
+/* Cumulative bytes the library itself copied host -> device (layer plans,
+ * hefv_ct_upload, hefv_key_upload) and device -> host (hefv_ct_download). */
+int hefv_transfer_stats(hefv_ctx* ctx, int64_t* h2d, int64_t* d2h);
+
 /* ---- measurement ---------------------------------------------------------
  * Integer-pipe throughput probe (roofline denominator; not a reference
  * function): kind 0 IMAD, 1 IMAD.HI, 2 IMAD.WIDE, 3 IADD3, 4 Shoup butterfly;

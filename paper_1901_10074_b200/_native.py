@@ -61,6 +61,27 @@ _SIGS = {
     "hefv_ks64_aux_setup": [_P, _I32],
     "hefv_ks64_aux_key": [_P, _P, _P, _P, _P, _P],
     "hefv_keyswitch64_aux": [_P, _P, _P, _P, _P, _I64, _P],
+    # object-level surface (api.cu) and the C++ layer planner (layer.cu)
+    "hefv_ct_alloc": [_P, _I32, _P],
+    "hefv_ct_free": [_P, _P],
+    "hefv_ct_upload": [_P, _P, _I32, _P, _P],
+    "hefv_ct_download": [_P, _P, _I32, _P, _P],
+    "hefv_key_upload": [_P, _P, _P, _P, _P],
+    "hefv_key_wrap": [_P, _P, _P, _P, _P],
+    "hefv_key_free": [_P],
+    "hefv_encrypt_slots": [_P, _P, _P, _P, _P, _P, _P, _I64, _P],
+    "hefv_decrypt_slots": [_P, _P, _I32, _P, _P, _P, _I64, _P],
+    "hefv_add": [_P, _P, _P, _I32, _P, _P],
+    "hefv_add_plain": [_P, _P, _I32, _P, _P, _P],
+    "hefv_cmult": [_P, _P, _I32, _P, _P, _P],
+    "hefv_rotate": [_P, _P, _U32, _P, _P, _P],
+    "hefv_mult": [_P, _P, _P, _P, _P, _P],
+    "hefv_layer_rows_work_words": [_P, _I32, _I64, _P, _I64, _P],
+    "hefv_layer_rows": [_P, _P, _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _I32,
+                        _P, _P, _P, _I32, _I64, _P, _I64, _P, _I64, _P],
+    "hefv_ks_timing": [_P, _I32],
+    "hefv_ks_stats": [_P, _P, _P, _P],
+    "hefv_transfer_stats": [_P, _P, _P],
 }
 
 EXPORTED = tuple(["hefv_last_error", "hefv_ctx_destroy", "hefv_launch_count"] + list(_SIGS))

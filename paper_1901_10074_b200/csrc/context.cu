@@ -32,6 +32,27 @@ int check_cuda(cudaError_t e, const char* where) {
   return -2;
 }
 
+static cudaEvent_t timing_event(hefv_ctx* c, cudaStream_t st) {
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+  cudaEventRecord(e, st);
+  c->ks_events.push_back(e);
+  return e;
+}
+void ks_begin(hefv_ctx* c, int64_t B, cudaStream_t st) {
+  c->ks_calls += 1;
+  c->ks_cts += B;
+  if (c->ks_timing) timing_event(c, st);
+}
+void ks_end(hefv_ctx* c, cudaStream_t st) {
+  if (c->ks_timing) timing_event(c, st);
+}
+static void drop_ks_events(hefv_ctx* c) {
+  for (cudaEvent_t e : c->ks_events)
+    if (e) cudaEventDestroy(e);
+  c->ks_events.clear();
+}
+
 typedef unsigned __int128 u128;
 
 static uint64_t mulmod(uint64_t a, uint64_t b, uint64_t m) { return (uint64_t)((u128)a * b % m); }
@@ -187,6 +208,18 @@ int hefv_ctx_create(hefv_ctx** out, uint32_t log_n, int32_t n32, const uint32_t*
     inf.mu = (uint64_t)(((u128)1 << 64) / p);
     c->info64.push_back(inf);
   }
+  // ---- stream-ordered temporaries of the object-level ops (api.cu) come from
+  // the device's default pool: keep freed blocks cached instead of returning
+  // them to the driver at every synchronisation (a rotation hop would
+  // otherwise map and unmap its key-switch scratch each call)
+  {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = 4ull << 30;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   // ---- upload
   cudaError_t e = cudaSuccess;
   auto up = [&](void** dst, const void* src, size_t bytes) {
@@ -228,7 +261,38 @@ void hefv_ctx_destroy(hefv_ctx* c) {
   cudaFree(c->d_ksa_j);
   cudaFree(c->d_ks64a_t);
   cudaFree(c->d_ks64a_j);
+  drop_ks_events(c);
+  if (c->stage_done) {
+    cudaEventSynchronize(c->stage_done);
+    cudaEventDestroy(c->stage_done);
+  }
+  if (c->h_stage) cudaFreeHost(c->h_stage);
   delete c;
+}
+
+int hefv_ks_timing(hefv_ctx* c, int32_t enable) {
+  if (!c) return fail("hefv_ks_timing: null context");
+  drop_ks_events(c);
+  c->ks_calls = c->ks_cts = 0;
+  c->ks_timing = enable != 0;
+  return 0;
+}
+
+int hefv_ks_stats(hefv_ctx* c, int64_t* calls, int64_t* cts, double* ms) {
+  if (!c) return fail("hefv_ks_stats: null context");
+  if (calls) *calls = c->ks_calls;
+  if (cts) *cts = c->ks_cts;
+  if (ms) {
+    double total = 0.0;
+    for (size_t i = 0; i + 1 < c->ks_events.size(); i += 2) {
+      HEFV_CUDA(cudaEventSynchronize(c->ks_events[i + 1]));
+      float t = 0.f;
+      HEFV_CUDA(cudaEventElapsedTime(&t, c->ks_events[i], c->ks_events[i + 1]));
+      total += t;
+    }
+    *ms = total;
+  }
+  return 0;
 }
 
 int hefv_fv_setup(hefv_ctx* c, int32_t k, int32_t a, int32_t t_index, const int32_t* slot_to_ev,

@@ -66,11 +66,6 @@ static int set_smem(K kern, size_t bytes) {
   return 0;
 }
 
-__device__ __forceinline__ uint32_t mont_canon(uint32_t x, const Prime32Info& inf) {
-  // x canonical -> x * 2^32 mod p canonical
-  uint32_t r = mont_mul_lazy(x, inf.r2, inf.p, inf.pinv_neg);
-  return r >= inf.p ? r - inf.p : r;
-}
 __device__ __forceinline__ uint32_t mulmod_small(uint32_t a, uint32_t b, const Prime32Info& inf) {
   return barrett62((uint64_t)a * b, inf.p, inf.mu);
 }

@@ -70,7 +70,27 @@ struct hefv_ctx {
   // the context are its aux primes
   int ks64a_T = 0;
   void* d_ks64a_t = nullptr;
-  void* d_ks64a_j = nullptr;  // key switch: 0 plain, 1 TMEM mask acc (E=16), 2 both accs in TMEM (E=32)
+  void* d_ks64a_j = nullptr;
+  // key-switch accounting (hefv_ks_stats): calls and ciphertexts always;
+  // with timing on, one CUDA event pair around every key-switch call
+  int64_t ks_calls = 0, ks_cts = 0;
+  bool ks_timing = false;
+  std::vector<cudaEvent_t> ks_events;  // (begin, end) pairs
+  // host -> device bytes copied by the library itself (plans, uploads)
+  int64_t h2d_bytes = 0, d2h_bytes = 0;
+  // pinned staging of the layer planner's host plan (hefv_layer_rows)
+  void* h_stage = nullptr;
+  size_t h_stage_bytes = 0;
+  cudaEvent_t stage_done = nullptr;
+};
+
+// switch-key handle of the object-level C-ABI (api.cu)
+struct hefv_key {
+  hefv_ctx* ctx = nullptr;
+  uint32_t* body = nullptr;  // (k, k, N) [target j][digit i], device order, Montgomery form
+  uint32_t* mask = nullptr;
+  uint32_t* aux = nullptr;   // (3, 2k, k, N) aux-basis form, or null (per-prime key switch)
+  bool owns = false;
 };
 
 namespace hefv {
@@ -79,6 +99,9 @@ void set_error(const std::string& msg);
 int fail(const std::string& msg);
 int check_cuda(cudaError_t e, const char* where);
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+// key-switch call bracketing (context.cu): counts, and events when timing is on
+void ks_begin(hefv_ctx* c, int64_t B, cudaStream_t st);
+void ks_end(hefv_ctx* c, cudaStream_t st);
 }  // namespace hefv
 
 #define HEFV_CUDA(call)                                                     \

@@ -24,6 +24,12 @@ struct InfoOf<Mod64> {
   typedef Prime64Info I;
 };
 
+// x canonical -> x * 2^32 mod p, canonical (Montgomery form)
+__device__ __forceinline__ uint32_t mont_canon(uint32_t x, const Prime32Info& inf) {
+  uint32_t r = mont_mul_lazy(x, inf.r2, inf.p, inf.pinv_neg);
+  return r >= inf.p ? r - inf.p : r;
+}
+
 __device__ __forceinline__ int brev_n(int x, int logn) { return (int)(__brev((unsigned)x) >> (32 - logn)); }
 
 

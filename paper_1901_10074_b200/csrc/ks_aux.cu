@@ -784,6 +784,16 @@ int run_ksa_key(hefv_ctx* c, const uint32_t* kb, const uint32_t* km, uint32_t* k
     default: return fail("aux key switch: N must be 2^10 .. 2^14"); \
   }
 
+static int ksa_dispatch(hefv_ctx* c, const uint32_t* kaux, const uint32_t* digits,
+                        int64_t dig_stride, const int32_t* dig_slot, uint32_t ginv,
+                        uint32_t* out0, uint32_t* out1, int64_t out_stride, const int32_t* slot,
+                        const uint32_t* adA0, const uint32_t* adA1, int64_t adA_stride,
+                        const uint32_t* adB0, const uint32_t* adB1, int64_t adB_stride,
+                        uint32_t* scratch, int64_t scratch_cts, int64_t B, cudaStream_t st) {
+  HEFV_KSA_DISPATCH(run_ksa, c, kaux, digits, dig_stride, dig_slot, ginv, out0, out1, out_stride, slot, adA0,
+                    adA1, adA_stride, adB0, adB1, adB_stride, scratch, scratch_cts, B, st)
+}
+
 extern "C" {
 
 int hefv_ks_aux_setup(hefv_ctx* c, int32_t aux_base) {
@@ -868,8 +878,12 @@ int hefv_keyswitch_aux(hefv_ctx* c, const uint32_t* kaux, const uint32_t* digits
     for (int it = 0; it < 6; ++it) inv *= 2u - g * inv;
     ginv = inv & (two_n - 1u);
   }
-  HEFV_KSA_DISPATCH(run_ksa, c, kaux, digits, dig_stride, dig_slot, ginv, out0, out1, out_stride, slot, adA0,
-                    adA1, adA_stride, adB0, adB1, adB_stride, scratch, scratch_cts, B, st)
+  ks_begin(c, B, st);
+  const int r = ksa_dispatch(c, kaux, digits, dig_stride, dig_slot, ginv, out0, out1, out_stride,
+                             slot, adA0, adA1, adA_stride, adB0, adB1, adB_stride, scratch,
+                             scratch_cts, B, st);
+  ks_end(c, st);
+  return r;
 }
 
 }  // extern "C"

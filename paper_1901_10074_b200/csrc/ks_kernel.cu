@@ -213,11 +213,14 @@ extern "C" int hefv_keyswitch(hefv_ctx* c, const uint32_t* kbody, const uint32_t
   if (!c || !c->fv_ready) return fail("hefv_keyswitch: context without FV setup");
   if (B <= 0) return 0;
   cudaStream_t st = as_stream(stream);
+  ks_begin(c, B, st);
+  int r;
   switch (c->log_n) {
 #define HEFV_KS(L)                                                                              \
   case L:                                                                                       \
-    return run_ks<L>(c, kbody, kmask, digits, dig_stride, out0, out1, out_stride, slot, adA0, \
-                     adA1, adA_stride, adB0, adB1, adB_stride, B, st);
+    r = run_ks<L>(c, kbody, kmask, digits, dig_stride, out0, out1, out_stride, slot, adA0,    \
+                  adA1, adA_stride, adB0, adB1, adB_stride, B, st);                             \
+    break;
     HEFV_KS(4)
     HEFV_KS(5)
     HEFV_KS(6)
@@ -231,6 +234,8 @@ extern "C" int hefv_keyswitch(hefv_ctx* c, const uint32_t* kbody, const uint32_t
     HEFV_KS(14)
 #undef HEFV_KS
     default:
-      return fail("hefv_keyswitch: unsupported N");
+      r = fail("hefv_keyswitch: unsupported N");
   }
+  ks_end(c, st);
+  return r;
 }

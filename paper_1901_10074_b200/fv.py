@@ -151,6 +151,16 @@ class FvContext:
             "hefv_fv_setup")
         if self.ks_aux:
             nat.check(lib.hefv_ks_aux_setup(h, self.k + self.a), "hefv_ks_aux_setup")
+        # everything the three setup calls received, for hosts that drive the
+        # C-ABI without this module (tests/c_host)
+        self.setup_record = {
+            "log_n": self.log_n, "primes32": primes32, "psi32": psi32, "primes64": [fp.t],
+            "psi64": [psi_t], "k": self.k, "a": self.a, "t_index": 0, "slot_to_ev": s2e,
+            "wq": qc.words, "q": qc.prod_words, "qhalf": qc.half_words,
+            "qhat": qc.hat_words.reshape(-1), "qhat_inv": qc.hat_inv, "wm": mc.words,
+            "m": mc.prod_words, "mhalf": mc.half_words, "mhat": mc.hat_words.reshape(-1),
+            "mhat_inv": mc.hat_inv, "delta_mod": self.delta_mod,
+            "ks_aux_base": self.k + self.a if self.ks_aux else -1}
         # gadget_i mod q_j table (k x k)
         gtab = np.array([[g % p for p in self.q_primes] for g in self.gadget], dtype=np.int64)
         self.d_gadget = nat.to_device(gtab.astype(np.int32))
@@ -296,6 +306,27 @@ class SwitchKey:
                                        device="cuda")
             ctx.call("hefv_ks_aux_key", body_dev.data_ptr(), mask_dev.data_ptr(),
                      self.aux_dev.data_ptr(), ctx.stream())
+        self._handle = None
+
+    @property
+    def handle(self):
+        """The C-ABI ``hefv_key*`` over this key's device buffers
+        (hefv_key_wrap; the tensors stay owned by this object)."""
+        if self._handle is None:
+            import ctypes as C
+
+            h = C.c_void_p()
+            aux = self.aux_dev.data_ptr() if self.aux_dev is not None else None
+            self._ctx.call("hefv_key_wrap", self.body_dev.data_ptr(), self.mask_dev.data_ptr(),
+                           aux, C.byref(h))
+            self._handle = h
+        return self._handle
+
+    def __del__(self):
+        h = getattr(self, "_handle", None)
+        if h is not None and nat._lib is not None:
+            nat._lib.hefv_key_free(h)
+            self._handle = None
 
     def _host(self, dev):
         """Device layout -> reference layout: Montgomery form undone on the
@@ -633,11 +664,11 @@ class FvBackend(SlotBackend):
             u[b] = ctx.rand_ternary(self.rng)
             e1[b] = ctx.rand_error(self.rng)
             e2[b] = ctx.rand_error(self.rng)
-        dm = self._delta_m_dev(np.stack([np.asarray(v) for v in vecs]))
+        slots = self._slots_dev(np.stack([np.asarray(v) for v in vecs]))
         out = ctx.empty(B, 2, ctx.k, ctx.n)
         ud, e1d, e2d = (nat.to_device(x) for x in (u, e1, e2))
-        ctx.call("hefv_encrypt", self._pk_mont.data_ptr(), ud.data_ptr(), e1d.data_ptr(),
-                 e2d.data_ptr(), dm.data_ptr(), out.data_ptr(), B, ctx.stream())
+        ctx.call("hefv_encrypt_slots", self._pk_mont.data_ptr(), ud.data_ptr(), e1d.data_ptr(),
+                 e2d.data_ptr(), slots.data_ptr(), out.data_ptr(), B, ctx.stream())
         return [self._fresh(out[b], 0) for b in range(B)]
 
     def _decrypt_poly_dev(self, devs):
@@ -656,8 +687,18 @@ class FvBackend(SlotBackend):
         """Plaintext polynomial mod t (fv.py:337-349)."""
         return self._host_plain(self._decrypt_poly_dev([self.dev(ct)])[0])
 
+    def _decrypt_slots_dev(self, devs):
+        ctx = self.ctx
+        torch = _torch()
+        nparts = devs[0].shape[0]
+        cts = torch.stack(devs) if len(devs) > 1 else devs[0][None]
+        out = ctx.empty(cts.shape[0], ctx.n // 2, dtype=torch.int64)
+        ctx.call("hefv_decrypt_slots", cts.data_ptr(), nparts, self._s_mont.data_ptr(),
+                 self._s2_mont.data_ptr(), out.data_ptr(), cts.shape[0], ctx.stream())
+        return out
+
     def _decrypt(self, ct):
-        slots = self._decode_dev(self._decrypt_poly_dev([self.dev(ct)]))[0]
+        slots = self._decrypt_slots_dev([self.dev(ct)])[0]
         return np.asarray(self._host_plain(slots), dtype=self._dtype)
 
     def decrypt_many(self, cts) -> list:
@@ -671,43 +712,48 @@ class FvBackend(SlotBackend):
             groups.setdefault(ct.nparts, []).append(i)
         res = [None] * len(cts)
         for _, idx in groups.items():
-            slots = self._decode_dev(self._decrypt_poly_dev([self.dev(cts[i]) for i in idx]))
+            slots = self._decrypt_slots_dev([self.dev(cts[i]) for i in idx])
             host = nat.to_host(slots)
             for r, i in enumerate(idx):
                 res[i] = np.asarray(host[r] if self.ctx.t < (1 << 31) else host[r].astype(object),
                                     dtype=self._dtype)
         return res
 
+    # The primitives below are single calls of the object-level C-ABI
+    # (api.cu): the Python side only allocates the output and passes pointers.
     def _add(self, a, b, level):
         da, db = self.dev(a), self.dev(b)
         m = min(da.shape[0], db.shape[0])
-        out = self.ctx.elementwise(0, da[:m].contiguous(), db[:m].contiguous())
+        da, db = da[:m].contiguous(), db[:m].contiguous()
+        out = _torch().empty_like(da)
+        self.ctx.call("hefv_add", da.data_ptr(), db.data_ptr(), m, out.data_ptr(),
+                      self.ctx.stream())
         return self._fresh(out, level)
 
     def _add_plain(self, a, vec, level):
-        dm = self._delta_m_dev(np.asarray(vec)[None])
-        da = self.dev(a)
-        out = da.clone()
-        out[0] = self.ctx.elementwise(0, da[0].contiguous(), dm[0])
+        slots = self._slots_dev(np.asarray(vec)[None])
+        da = self.dev(a).contiguous()
+        out = _torch().empty_like(da)
+        self.ctx.call("hefv_add_plain", da.data_ptr(), da.shape[0], slots.data_ptr(),
+                      out.data_ptr(), self.ctx.stream())
         return self._fresh(out, level)
 
     def _cmult(self, a, vec, level):
-        m = self._cmult_plain_dev(np.asarray(vec)[None])
-        da = self.dev(a)
+        slots = self._slots_dev(np.asarray(vec)[None])
+        da = self.dev(a).contiguous()
         out = _torch().empty_like(da)
-        self.ctx.call("hefv_mul_plain", da.data_ptr(), m.data_ptr(), out.data_ptr(), 1,
-                      da.shape[0], 1, self.ctx.stream())
+        self.ctx.call("hefv_cmult", da.data_ptr(), da.shape[0], slots.data_ptr(), out.data_ptr(),
+                      self.ctx.stream())
         return self._fresh(out, level)
 
     def _mult(self, a, b, level):
         ctx = self.ctx
-        da = self.dev(a).contiguous()
-        db = da if b is a else self.dev(b).contiguous()
-        out3 = ctx.empty(3, ctx.k, ctx.n)
-        scratch = ctx.empty(7 * ctx.a * ctx.n)
-        ctx.call("hefv_mult_tensor", da.data_ptr(), db.data_ptr(), out3.data_ptr(),
-                 scratch.data_ptr(), ctx.stream())
-        return self._relinearize(out3, level)
+        da = self.dev(a)[:2].contiguous()
+        db = da if b is a else self.dev(b)[:2].contiguous()
+        out = ctx.empty(2, ctx.k, ctx.n)
+        ctx.call("hefv_mult", da.data_ptr(), db.data_ptr(), self.keys.relin.handle,
+                 out.data_ptr(), ctx.stream())
+        return self._fresh(out, level)
 
     def _square_many_dev(self, devs, chunk=512):
         """Squares of B ciphertexts (device stacks), batched: one tensor launch
@@ -736,16 +782,6 @@ class FvBackend(SlotBackend):
             res += [out[i] for i in range(B)]
         return res
 
-    def _relinearize(self, out3, level):
-        from .planner import keyswitch_call
-
-        ctx = self.ctx
-        out = ctx.empty(2, ctx.k, ctx.n)
-        key = self.keys.relin
-        keyswitch_call(ctx, key, out3[2].data_ptr(), 0, out[0].data_ptr(), out[1].data_ptr(), 0,
-                       None, out3[0].data_ptr(), out3[1].data_ptr(), 0, None, None, 0, 1)
-        return self._fresh(out, level)
-
     def rotation_hops(self, offset: int) -> list:
         """Key-switch hops of a rotation (fv.py:422-425)."""
         if offset == 0:
@@ -755,14 +791,10 @@ class FvBackend(SlotBackend):
         return [1 << j for j in range(offset.bit_length()) if offset >> j & 1]
 
     def _hop(self, dev, off):
-        from .planner import rotation_keyswitch
-
         ctx = self.ctx
-        scratch = ctx.empty(2, ctx.k, ctx.n)
         out = ctx.empty(2, ctx.k, ctx.n)
-        rotation_keyswitch(ctx, self.keys.galois[off], dev.data_ptr(), 0, None,
-                           galois_element(off, ctx.n), 1, out[0].data_ptr(), out[1].data_ptr(), 0,
-                           None, None, None, 0, scratch.data_ptr())
+        ctx.call("hefv_rotate", dev.data_ptr(), galois_element(off, ctx.n),
+                 self.keys.galois[off].handle, out.data_ptr(), ctx.stream())
         return out
 
     def _rotate(self, a, offset, level):

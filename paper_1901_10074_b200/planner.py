@@ -24,6 +24,10 @@ planner evaluates a tile of T rows per kernel launch:
      reference's order;
   6. per-output-ciphertext modular sums of the pieces (hefv_accumulate_rows).
 
+Steps 1-6 run in C++ (hefv_layer_rows, csrc/layer.cu) from one call per
+layer: this module builds the host plan (CSR plaintexts, per-row output /
+offset / bias), sizes the workspaces, checks depths and replays the ledger.
+
 Every ciphertext the planner produces has exactly the limbs the serial
 schedule produces (the key-switch noise depends only on the ciphertext being
 switched, which is the same), the Generator is consumed exactly as in the
@@ -37,49 +41,44 @@ import numpy as np
 
 from . import _native as nat
 from .errors import DepthBudgetError
-from .ring import galois_element
 
 _TILE_BYTES = 24 << 30  # device memory budget for one tile's working set
 
-# Instrumentation read by bench.py: key-switch launches / ciphertexts, and
-# (when KS_EVENTS is a list) CUDA event pairs bracketing every key-switch
-# launch on the launching stream.
-STATS = {"ks_launches": 0, "ks_cts": 0}
-KS_EVENTS = None
-
 
 def keyswitch_call(ctx, key, *args, dig_slot=None, galois=0):
-    """One batched key switch under ``key`` (a SwitchKey) with the planner's
-    accounting; ``args`` are hefv_keyswitch's after the key pointers (the
-    batch size last).  Keys with an aux-basis form go through
-    hefv_keyswitch_aux (same limbs, fewer transforms), which can also read
-    the digit rows through a slot map and apply a Galois automorphism on the
-    fly (``dig_slot`` device pointer, ``galois`` element); the per-prime
-    kernel needs its digits materialised."""
-    import torch
-
+    """One batched key switch under ``key`` (a SwitchKey); ``args`` are
+    hefv_keyswitch's after the key pointers (the batch size last).  Keys with
+    an aux-basis form go through hefv_keyswitch_aux (same limbs, fewer
+    transforms), which can also read the digit rows through a slot map and
+    apply a Galois automorphism on the fly (``dig_slot`` device pointer,
+    ``galois`` element); the per-prime kernel needs its digits materialised.
+    Calls and ciphertexts are counted by the library (``ks_stats``)."""
     batch = int(args[-1])
-    STATS["ks_launches"] += 1
-    STATS["ks_cts"] += batch
     if key.aux_dev is not None:
         scratch, cap = _ks_workspace(ctx, batch)
-        name = "hefv_keyswitch_aux"
-        full = (key.aux_dev.data_ptr(), args[0], args[1], dig_slot, int(galois), *args[2:-1],
-                scratch.data_ptr(), cap, batch)
+        ctx.call("hefv_keyswitch_aux", key.aux_dev.data_ptr(), args[0], args[1], dig_slot,
+                 int(galois), *args[2:-1], scratch.data_ptr(), cap, batch, ctx.stream())
     else:
         if dig_slot is not None or galois:
             raise ValueError("the per-prime key switch needs materialised digits")
-        name = "hefv_keyswitch"
-        full = (key.body_dev.data_ptr(), key.mask_dev.data_ptr(), *args)
-    if KS_EVENTS is not None:
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        ctx.call(name, *full, ctx.stream())
-        e1.record()
-        KS_EVENTS.append((e0, e1, batch))
-    else:
-        ctx.call(name, *full, ctx.stream())
+        ctx.call("hefv_keyswitch", key.body_dev.data_ptr(), key.mask_dev.data_ptr(), *args,
+                 ctx.stream())
+
+
+def ks_reset(ctx, timing: bool = False) -> None:
+    """Zero the library's key-switch counters of ``ctx``; with ``timing`` a
+    CUDA event pair brackets every later key-switch call (hefv_ks_timing)."""
+    ctx.call("hefv_ks_timing", 1 if timing else 0)
+
+
+def ks_stats(ctx) -> dict:
+    """Key-switch calls, ciphertexts and (with timing on) summed device ms
+    since the last ``ks_reset`` (hefv_ks_stats; synchronises on the events)."""
+    import ctypes as C
+
+    calls, cts, ms = C.c_int64(), C.c_int64(), C.c_double()
+    ctx.call("hefv_ks_stats", C.byref(calls), C.byref(cts), C.byref(ms))
+    return {"ks_launches": calls.value, "ks_cts": cts.value, "ks_ms": ms.value}
 
 
 def rotation_keyswitch(ctx, key, src, src_stride, slot, g, B, out0, out1, out_stride, out_slot,
@@ -366,114 +365,54 @@ def _tile_rows(backend, n_plain_per_row: float) -> int:
 
 def _run_rows(backend, rows, x, seg_lists, active, m_arr, off_arr, bias_arr, out_dev, n_iter,
               skip_zero_segments):
+    """The device work of a layer: one hefv_layer_rows call (layer.cu) over
+    the active rows, grouped by output ciphertext.  Python only builds the
+    host plan (CSR plaintexts, per-row output / offset / bias) and the
+    workspaces; tiling, AllSum, biases, the e0 mask, placement hops and the
+    output sums run in C++."""
+    import ctypes as C
+
     import torch
 
     ctx = backend.ctx
-    kq, n = ctx.k, ctx.n
     s = x.slots_used
     t = backend.params.plain_modulus
-    st = ctx.stream()
-    stack = kq * n
-    ct_words = 2 * stack
-    # NTT (device order, Montgomery form) of the layer inputs, once per layer
     xin = torch.stack([backend.dev(ct)[:2] for ct in x.cts]).contiguous()
-    x_ntt = ctx.to_mont(ctx.ntt_q(xin.view(-1, kq, n)).view_as(xin))
-
-    # rows grouped by output ciphertext (stable), so each tile's pieces are contiguous per m
     order = active[np.argsort(m_arr[active], kind="stable")]
+    R = len(order)
     avg_plain = max(1.0, float(np.mean([len(seg_lists[i]) for i in order])))
     T = _tile_rows(backend, avg_plain)
-    e0 = backend.e0_plain_ntt()
-    keys = backend.keys.galois
-    slot_count = backend.params.slot_count
-
     plan = _sparse_plan(rows, order, s, t)
-    up = nat.to_device_async
+    row_out = np.ascontiguousarray(m_arr[order], dtype=np.int32)
+    row_off = np.ascontiguousarray(off_arr[order], dtype=np.int32)
+    row_bias = np.array([int(bias_arr[i]) % t for i in order], dtype=np.uint64)
+    row_ptr = np.ascontiguousarray(plan["row_ptr"], dtype=np.int64)
+    plain_ptr = np.ascontiguousarray(plan["ptr"], dtype=np.int64)
+    plain_seg = np.ascontiguousarray(plan["seg"], dtype=np.int32)
+    slot_idx = np.ascontiguousarray(plan["slot"], dtype=np.int32)
+    slot_val = np.ascontiguousarray(plan["val"], dtype=np.uint64)
+    galois = backend.keys.galois
+    offsets = np.array(sorted(galois), dtype=np.int32)
+    handles = (C.c_void_p * len(offsets))(*[galois[int(o)].handle.value for o in offsets])
 
-    for t0 in range(0, len(order), T):
-        tile = order[t0:t0 + T]
-        B = len(tile)
-        # ---- 1. sparse plaintexts of every (row, nonzero segment) -------------
-        g_lo, g_hi = plan["row_ptr"][t0], plan["row_ptr"][t0 + B]
-        e_lo, e_hi = plan["ptr"][g_lo], plan["ptr"][g_hi]
-        P = int(g_hi - g_lo)
-        ptr = plan["ptr"][g_lo:g_hi + 1] - e_lo
-        slot_idx = [plan["slot"][e_lo:e_hi]]
-        vals = [plan["val"][e_lo:e_hi]]
-        row_ptr = plan["row_ptr"][t0:t0 + B + 1] - g_lo
-        plain_seg = plan["seg"][g_lo:g_hi]
-        acc = torch.empty((B, 2, kq, n), dtype=torch.int32, device="cuda")
-        if P:
-            d_ptr = up(np.asarray(ptr, dtype=np.int32))
-            d_idx = up(np.concatenate(slot_idx).astype(np.int32))
-            d_val = up(np.concatenate(vals).view(np.int64))
-            polys = torch.empty((P, n), dtype=torch.int64, device="cuda")
-            ctx.call("hefv_encode_sparse", d_ptr.data_ptr(), d_idx.data_ptr(), d_val.data_ptr(),
-                     polys.data_ptr(), P, st)
-            m_ntt = torch.empty((P, kq, n), dtype=torch.int32, device="cuda")
-            ctx.call("hefv_plain_to_rns", polys.data_ptr(), m_ntt.data_ptr(), P, 1, 1, 0, st)
-            del polys
-            d_rp = up(np.asarray(row_ptr, dtype=np.int32))
-            d_ps = up(np.asarray(plain_seg, dtype=np.int32))
-            ctx.call("hefv_rows_mac", x_ntt.data_ptr(), m_ntt.data_ptr(), d_rp.data_ptr(),
-                     d_ps.data_ptr(), acc.data_ptr(), B, st)
-            del m_ntt
-        else:
-            acc.zero_()
-        # ---- 3. AllSum over s slots ----------------------------------------------
-        scr = torch.empty_like(acc)
-        a0 = acc.data_ptr()
-        a1 = a0 + stack * 4
-        s0 = scr.data_ptr()
-        for j in range(n_iter):
-            shift = 1 << j
-            key = keys[shift]
-            g = galois_element(shift, n)
-            rotation_keyswitch(ctx, key, a0, ct_words, None, g, B, a0, a1, ct_words, None, a0, a1,
-                               ct_words, s0)
-        # ---- 4. biases and the e0 mask ---------------------------------------------
-        bias_rows = [bi for bi, i in enumerate(tile) if bias_arr[i]]
-        if bias_rows:
-            nb = len(bias_rows)
-            d_ptr = torch.arange(nb + 1, dtype=torch.int32, device="cuda")
-            d_idx = torch.zeros(nb, dtype=torch.int32, device="cuda")
-            bv = np.array([bias_arr[tile[bi]] % t for bi in bias_rows], dtype=np.uint64)
-            d_val = up(bv.view(np.int64))
-            polys = torch.empty((nb, n), dtype=torch.int64, device="cuda")
-            ctx.call("hefv_encode_sparse", d_ptr.data_ptr(), d_idx.data_ptr(), d_val.data_ptr(),
-                     polys.data_ptr(), nb, st)
-            dm = torch.empty((nb, kq, n), dtype=torch.int32, device="cuda")
-            ctx.call("hefv_plain_to_rns", polys.data_ptr(), dm.data_ptr(), nb, 0, 0, 0, st)
-            d_slot = up(np.asarray(bias_rows, dtype=np.int32))
-            ctx.call("hefv_add_part0", a0, ct_words, d_slot.data_ptr(), dm.data_ptr(), nb, st)
-        ctx.call("hefv_mul_plain", a0, e0.data_ptr(), a0, B, 2, 1, st)
-        # ---- 5. placement rotations by -off ------------------------------------------
-        hop_groups: dict = {}
-        for bi, i in enumerate(tile):
-            off = int(off_arr[i])
-            if not off:
-                continue
-            rot = (-off) % slot_count
-            for h in backend.rotation_hops(rot):
-                hop_groups.setdefault(h, []).append(bi)
-        # custom (non power-of-two) keys are single hops; power-of-two hops ascend
-        for h in sorted(hop_groups, key=lambda v: (v & (v - 1) == 0, v)):
-            idx = hop_groups[h]
-            d_slot = up(np.asarray(idx, dtype=np.int32))
-            nb = len(idx)
-            sub = scr[:nb]
-            b0 = sub.data_ptr()
-            key = keys[h]
-            rotation_keyswitch(ctx, key, a0, ct_words, d_slot.data_ptr(), galois_element(h, n), nb,
-                               a0, a1, ct_words, d_slot.data_ptr(), None, None, 0, b0)
-        del scr
-        # ---- 6. sum pieces into their output ciphertexts -----------------------------
-        ms = m_arr[tile]
-        bounds = np.flatnonzero(np.diff(ms)) + 1
-        seg = np.concatenate([[0], bounds, [B]]).astype(np.int32)
-        seg_out = ms[seg[:-1]].astype(np.int32)
-        d_seg = up(seg)
-        d_out = up(seg_out)
-        ctx.call("hefv_accumulate_rows", a0, d_seg.data_ptr(), d_out.data_ptr(),
-                 out_dev.data_ptr(), len(seg_out), 1, st)
-        del acc
+    def ptr(a):
+        return a.ctypes.data if a.size else None
+
+    words = C.c_int64()
+    ctx.call("hefv_layer_rows_work_words", len(x.cts), R, ptr(row_ptr), T, C.byref(words))
+    work = torch.empty(words.value, dtype=torch.int32, device="cuda")
+    if ctx.ks_aux:
+        ws, cap = _ks_workspace(ctx, T)
+        ws_ptr = ws.data_ptr()
+    else:
+        ws_ptr, cap = None, 0
+    h2d0 = C.c_int64()
+    ctx.call("hefv_transfer_stats", C.byref(h2d0), None)
+    ctx.call("hefv_layer_rows", xin.data_ptr(), len(x.cts), R, ptr(row_out), ptr(row_off),
+             ptr(row_bias), ptr(row_ptr), ptr(plain_seg), ptr(plain_ptr), ptr(slot_idx),
+             ptr(slot_val), n_iter, backend.params.slot_count, len(offsets), ptr(offsets),
+             handles, out_dev.data_ptr(), out_dev.shape[0], T, work.data_ptr(), words.value,
+             ws_ptr, cap, ctx.stream())
+    h2d1 = C.c_int64()
+    ctx.call("hefv_transfer_stats", C.byref(h2d1), None)
+    nat.TRAFFIC["h2d"] += h2d1.value - h2d0.value   # the plan, staged and copied by the library

@@ -38,7 +38,7 @@ lat = []
 ok = True
 for img in images:
     torch.cuda.synchronize()
-    planner.STATS.update(ks_launches=0, ks_cts=0)
+    planner.ks_reset(be.ctx)
     a = time.perf_counter()
     out = I.infer(be, net, I.pack_image(be, img))
     logits = I.decrypt_logits(be, out)
@@ -46,9 +46,10 @@ for img in images:
     lat.append(time.perf_counter() - a)
     want = centred_mod(plaintext_forward(net, img), params.plain_modulus)
     ok = ok and [int(v) for v in logits] == want
+    ks = planner.ks_stats(be.ctx)
 res.update({"latency_s": [round(x, 3) for x in lat], "images_per_s": round(len(lat) / sum(lat), 5),
-            "logits_equal_exact_plaintext_mod_t": ok, "ks_launches_per_image": planner.STATS["ks_launches"],
-            "ks_cts_per_image": planner.STATS["ks_cts"],
+            "logits_equal_exact_plaintext_mod_t": ok, "ks_launches_per_image": ks["ks_launches"],
+            "ks_cts_per_image": ks["ks_cts"],
             "cost_report": be.cost_report().as_dict(),
             "serial_op_counts": workload_op_counts(cfg if cfg != 5 else 2)})
 print(json.dumps(res), flush=True)
