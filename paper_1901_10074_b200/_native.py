@@ -137,13 +137,10 @@ def launch_count() -> int:
 
 
 def to_device(arr):
-    """numpy -> CUDA tensor (counted as host-to-device traffic)."""
-    import numpy as np
-    import torch
-
-    a = np.ascontiguousarray(arr)
-    TRAFFIC["h2d"] += a.nbytes
-    return torch.from_numpy(a).cuda()
+    """numpy -> CUDA tensor (counted as host-to-device traffic), staged
+    through pinned memory and asynchronous on the current stream: a pageable
+    copy would make the host wait for every launch queued before it."""
+    return to_device_async(arr)
 
 
 def to_device_async(arr):

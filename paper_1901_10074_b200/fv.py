@@ -701,6 +701,30 @@ class FvBackend(SlotBackend):
         slots = self._decrypt_slots_dev([self.dev(ct)])[0]
         return np.asarray(self._host_plain(slots), dtype=self._dtype)
 
+    def decrypt_slots_async(self, cts):
+        """Queue the decryption of ``cts`` (same part count) and an
+        asynchronous copy of the slots to pinned host memory; returns a
+        callable that waits for that copy only (not for later launches) and
+        gives the slot vectors.  Lets a stream of images decrypt image i
+        while image i+1 is already queued."""
+        torch = _torch()
+        for ct in cts:
+            self._check_params(ct)
+        dev = self._decrypt_slots_dev([self.dev(ct) for ct in cts])
+        host = torch.empty(dev.shape, dtype=dev.dtype, pin_memory=True)
+        host.copy_(dev, non_blocking=True)
+        nat.TRAFFIC["d2h"] += host.numel() * host.element_size()
+        done = torch.cuda.Event()
+        done.record()
+
+        def wait():
+            done.synchronize()
+            arr = host.numpy()
+            return [np.asarray(arr[i] if self.ctx.t < (1 << 31) else arr[i].astype(object),
+                               dtype=self._dtype) for i in range(arr.shape[0])]
+
+        return wait
+
     def decrypt_many(self, cts) -> list:
         """Batched decryption of several ciphertexts (one launch per stage)."""
         if not cts:
