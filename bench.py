@@ -14,9 +14,10 @@ the 126 MB L2, so no explicit flush is needed.
 
 Further legs on the same line (N = 1): `config3` -- one 256x256x3 image end
 to end (keygen excluded, logits checked), `config5` -- images/s over a
-stream of 8 ROP images (one key, one Generator, logits checked),
-`ntt_microbench` -- config 4, and `cpu_baseline` -- the reference itself
-(hepack + numba from baseline/_ref) on a bounded sample, extrapolated.
+stream of 8 ROP images (one key, one Generator, logits checked), `config1`
+-- the toy desk net end to end, `ntt_microbench` -- config 4, and
+`cpu_baseline` -- the reference itself (hepack + numba from baseline/_ref) on
+a bounded sample, extrapolated, plus config 1 measured in full.
 
 Multi-GPU: the path does not shard (north star: one GPU); N ranks run N
 independent replicas, timed as the max over ranks, `scaling: "weak"`.
@@ -24,7 +25,8 @@ independent replicas, timed as the max over ranks, `scaling: "weak"`.
 --impl reference runs the unmodified reference (baseline/_ref, its own
 keygen and FvBackend) on the host CPU: per step, a bounded sample of its
 operations in one process (-> single-image latency, extrapolated with the
-exact serial op counts) and in P worker processes (-> images/s).
+exact serial op counts) and in P worker processes (-> images/s); config 1
+is also run in full once.
 """
 
 from __future__ import annotations
@@ -240,6 +242,7 @@ def run_ours(args, rank, local_rank, world):
         del be, pv, out
         torch.cuda.empty_cache()
         legs["config3"], be3 = _config3_leg()
+        legs["config1"] = _config1_leg()
 
     result = None
     if rank == 0:
@@ -373,6 +376,40 @@ def _config5_leg(be, net, count: int) -> dict:
                     f"{count} images (same key, one Generator), CUDA events around the stream"}
 
 
+def _config1_leg() -> dict:
+    """Config 1 (BASELINE configs[0], the reference's CPU-runnable toy net at
+    desk) end to end through the public API: keygen (reported apart), then
+    pack_image -> infer -> decrypt_logits, CUDA events around the three.  The
+    reference's own run of the same thing is measured in full by the
+    cpu_baseline leg (config1_measured_in_full)."""
+    import torch
+
+    from paper_1901_10074_b200 import inference as I
+    from paper_1901_10074_b200.configs import (KEY_SEED, centred_mod, config_network,
+                                               config_params, plaintext_forward)
+    from paper_1901_10074_b200.fv import FvBackend
+
+    params = config_params(1)
+    img, net = config_network(1)
+    t0 = time.perf_counter()
+    be = FvBackend(params, rng=np.random.default_rng(KEY_SEED))
+    torch.cuda.synchronize()
+    keygen_s = time.perf_counter() - t0
+    I.decrypt_logits(be, I.infer(be, net, I.pack_image(be, img)))  # warm-up (plans, caches)
+    be = FvBackend(params, rng=np.random.default_rng(KEY_SEED))    # fresh Generator: same draws
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    logits = I.decrypt_logits(be, I.infer(be, net, I.pack_image(be, img)))
+    e1.record()
+    torch.cuda.synchronize()
+    want = centred_mod(plaintext_forward(net, img), params.plain_modulus)
+    return {"ms": round(e0.elapsed_time(e1), 2), "keygen_s": round(keygen_s, 2),
+            "logits": [int(v) for v in logits],
+            "logits_exact": [int(v) for v in logits] == want,
+            "path": "pack_image(host pixels) + infer + decrypt_logits(host logits), desk, 1 image"}
+
+
 def _config3_leg():
     """Config 3 (BASELINE configs[2]): one 256x256x3 image end to end through
     the public API -- pack_image (host pixels) -> infer (conv1, square, conv2,
@@ -485,6 +522,7 @@ def _cpu_baseline(params, counts, gpu_keys) -> dict:
                         "setup_s": round(setup, 2), "op_counts": cnt}
         del be, st
     ntt = RB.ntt_object_path(H)
+    c1 = RB.config1_full(H)
     c2 = per_cfg[2]
     return {"value": c2["ms"], "unit": "ms", "cores": 1, "kind": "reference",
             "sample": "hepack (the reference, baseline/_ref, numba "
@@ -493,6 +531,7 @@ def _cpu_baseline(params, counts, gpu_keys) -> dict:
                       "retina; single-image latency = sum_op exact serial count x time "
                       "(extrapolated: a whole image is ~30 h of CPU)",
             "config3_ms": per_cfg.get(3, {}).get("ms"),
+            "config1_measured_in_full": c1,
             "per_config": per_cfg,
             "config4_object_ntt_polys_per_s": ntt,
             "cpu": info, "wall_s": round(time.perf_counter() - t_all, 1)}
@@ -517,7 +556,9 @@ def _ntt_microbench(peaks=None):
     """Config 4 secondary: batched forward/inverse NTT polys/s (device order),
     with each entry's roofline fraction: per-limb work (N/2) log2 N + N
     modmuls against the measured lazy Shoup butterfly rate of
-    the word size (32-bit or 64-bit)."""
+    the word size (32-bit or 64-bit) -- `frac` -- and against 8(d)'s literal
+    c x IMAD-rate model -- `frac_8d_literal` (which ignores that IMAD.HI and
+    IMAD.WIDE issue at half rate, so it understates what the pipe allows)."""
     import ctypes as C
 
     import torch
@@ -528,7 +569,8 @@ def _ntt_microbench(peaks=None):
     lib = nat.load()
     res, fracs = {}, {}
     for log_n, bits, L, batch in [(16, 60, 8, 64), (15, 55, 8, 128), (14, 60, 8, 256),
-                                  (13, 60, 8, 256), (12, 50, 8, 1024), (14, 30, 22, 256)]:
+                                  (13, 60, 8, 256), (12, 50, 8, 1024), (14, 30, 22, 256),
+                                  (12, 30, 8, 1024)]:
         n = 1 << log_n
         primes = find_ntt_primes(L, bits, 2 * n)
         psis = [root_of_unity(p, n) for p in primes]
@@ -564,8 +606,12 @@ def _ntt_microbench(peaks=None):
             if peaks:
                 pk = peaks["shoup_butterfly64" if wide else "shoup_butterfly"]
                 tm = ps * ((n // 2) * log_n + n) / 1e12
+                # SURVEY.md 8(d)'s literal constants: c IMAD per modmul (3 for
+                # 30-bit, 10 for a 64-bit twiddle modmul) at the probed IMAD rate
+                c8d = 10 if wide else 3
                 fracs[key] = {"Tmodmul_s": round(tm, 3), "peak": round(pk, 3),
-                              "frac": round(tm / pk, 3)}
+                              "frac": round(tm / pk, 3),
+                              "frac_8d_literal": round(tm * c8d / peaks["imad"], 3)}
         lib.hefv_ctx_destroy(h)
     out = {"unit": "limb-polys/s", **res}
     if peaks:
@@ -650,6 +696,7 @@ def run_reference(args, rank, world):
         thr.append(sum(1.0 / x for x in per_worker))
     value = statistics.mean(lat)
     ips = statistics.mean(thr)
+    c1 = RB.config1_full(H)
     sample = (f"hepack (baseline/_ref, numba {'on' if H.ntt._HAVE_NUMBA else 'off'}), own keygen; "
               "per step 1 key-switch hop + 1 cmult + 10 adds at retina in one process; "
               "square/encrypt/decrypt timed once; single-image latency extrapolated with the "
@@ -667,6 +714,7 @@ def run_reference(args, rank, world):
                                "sample timed in all of them at once): images/s = sum over "
                                "workers of 1 / latency under load"},
         "cpu": info,
+        "config1_measured_in_full": c1,
         "e2e": {"value": round(value, 1), "unit": "ms", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "keygen_s": round(keygen_s, 1),

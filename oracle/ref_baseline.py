@@ -194,3 +194,39 @@ def ntt_object_path(H, sizes=(12, 13, 14, 15, 16), bits=60, reps=1) -> dict:
         out[f"N=2^{log_n},{bits}-bit,fwd"] = round(1.0 / t_f, 2)
         out[f"N=2^{log_n},{bits}-bit,inv"] = round(1.0 / t_i, 2)
     return out
+
+
+def reference_network(H, cfg: int):
+    """The reference's own NetworkSpec objects for a config (the draws of
+    configs.config_network)."""
+    from paper_1901_10074_b200.configs import config_network
+
+    img, net = config_network(cfg)
+    R = H.inference
+    layers = []
+    for layer in net.layers:
+        kind = type(layer).__name__
+        if kind == "ConvSpec":
+            layers.append(R.ConvSpec(layer.filters, layer.kernel, layer.stride, layer.in_shape,
+                                     layer.weights, layer.biases))
+        elif kind == "FcSpec":
+            layers.append(R.FcSpec(layer.out_neurons, layer.weights, layer.biases))
+        else:
+            layers.append(R.SquareSpec())
+    return img, R.NetworkSpec(layers, net.input_shape)
+
+
+def config1_full(H, seed=1234) -> dict:
+    """Config 1 measured IN FULL on one core: the reference's own keygen
+    (untimed), then pack_image -> infer -> decrypt_logits exactly as its CLI
+    runs them (inference.py:178-452; cli.py:151-155)."""
+    img, net = reference_network(H, 1)
+    t0 = time.perf_counter()
+    be = reference_backend(H, 1, seed=seed)
+    keygen = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    logits = H.inference.decrypt_logits(be, H.inference.infer(be, net, H.inference.pack_image(
+        be, img)))
+    ms = (time.perf_counter() - t1) * 1000.0
+    return {"ms": round(ms, 1), "keygen_s": round(keygen, 2),
+            "logits": [int(v) for v in logits]}
