@@ -382,6 +382,7 @@ def _config1_leg() -> dict:
     pack_image -> infer -> decrypt_logits, CUDA events around the three.  The
     reference's own run of the same thing is measured in full by the
     cpu_baseline leg (config1_measured_in_full)."""
+    import numpy as np
     import torch
 
     from paper_1901_10074_b200 import inference as I
