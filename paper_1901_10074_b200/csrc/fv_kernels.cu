@@ -202,54 +202,36 @@ static int run_decode(hefv_ctx* c, const uint64_t* poly, uint64_t* slots, int64_
 // ---------------------------------------------------------------------------
 // plaintext poly mod t -> RNS stack (fv.py:291-310, fv.py:366-370)
 // ---------------------------------------------------------------------------
-template <int LOGN>
-__global__ void __launch_bounds__(Geo<LOGN, Loge32<LOGN>::v>::NT)
-    k_plain_to_rns(const uint64_t* __restrict__ poly, uint32_t* __restrict__ out, int k,
-                   uint64_t t, int mode, int to_ntt, int montgomery,
-                   const uint32_t* __restrict__ delta, const uint2* __restrict__ tw_all,
-                   const Prime32Info* __restrict__ info) {
-  constexpr int LE = Loge32<LOGN>::v;
-  typedef Geo<LOGN, LE> G_;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  uint32_t* sm = reinterpret_cast<uint32_t*>(smraw);
-  const int j = blockIdx.x;
-  const size_t b = blockIdx.y;
-  const Prime32Info inf = info[j];
-  const Mod32 md = make_mod(inf);
-  const uint64_t* src = poly + b * G_::N;
-  uint32_t* dst = out + (b * k + j) * (size_t)G_::N;
-  const int tid = threadIdx.x;
+// Residues first (one thread per coefficient, each u64 read once, the k
+// residue rows written coalesced), then the persistent batched transform
+// (k_ntt32_b: prime-major, twiddles staged in shared memory; in place) and,
+// when asked, the Montgomery form.  A per-(prime, plaintext) CTA that read
+// its twiddles from L2 ran at a third of the batched transform's rate.
+static unsigned grid_for(int64_t total, int threads);
+
+__global__ void k_plain_residues(const uint64_t* __restrict__ poly, uint32_t* __restrict__ out,
+                                 int64_t B, int k, int log_n, uint64_t t, int mode,
+                                 const uint32_t* __restrict__ delta,
+                                 const Prime32Info* __restrict__ info) {
+  const int64_t n = 1ll << log_n;
   const uint64_t half = t >> 1;
-  const uint32_t dj = delta[j];
-  uint32_t x[G_::E];
-#pragma unroll
-  for (int e = 0; e < G_::E; ++e) {
-    const uint64_t m = src[tid + e * G_::NT];
-    uint32_t v;
-    if (mode == 0) {
-      v = mulmod_small(barrett62(m, inf.p, inf.mu), dj, inf);
-    } else if (m > half) {
-      const uint32_t r = barrett62(t - m, inf.p, inf.mu);
-      v = r ? inf.p - r : 0u;
-    } else {
-      v = barrett62(m, inf.p, inf.mu);
-    }
-    x[e] = v;
-  }
-  if (to_ntt) {
-    cta_fwd<LOGN, LE, Mod32>(md, x, sm, tw_all + (size_t)j * G_::N);
-#pragma unroll
-    for (int e = 0; e < G_::E; ++e) {
-      uint32_t v = md.canon4(x[e]);
-      if (montgomery) v = mont_canon(v, inf);
-      dst[row_index<LOGN, LE>(tid, e)] = v;
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < G_::E; ++e) {
-      uint32_t v = x[e];
-      if (montgomery) v = mont_canon(v, inf);
-      dst[tid + e * G_::NT] = v;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < B * n;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = g >> log_n, i = g & (n - 1);
+    const uint64_t m = poly[g];
+    uint32_t* dst = out + b * k * n + i;
+    for (int j = 0; j < k; ++j) {
+      const Prime32Info inf = info[j];
+      uint32_t v;
+      if (mode == 0) {
+        v = mulmod_small(barrett62(m, inf.p, inf.mu), delta[j], inf);  // Delta m, m uncentred
+      } else if (m > half) {
+        const uint32_t r = barrett62(t - m, inf.p, inf.mu);  // centred m < 0
+        v = r ? inf.p - r : 0u;
+      } else {
+        v = barrett62(m, inf.p, inf.mu);
+      }
+      dst[(int64_t)j * n] = v;
     }
   }
 }
@@ -258,13 +240,14 @@ template <int LOGN>
 static int run_plain_to_rns(hefv_ctx* c, const uint64_t* poly, uint32_t* out, int64_t B, int mode,
                             int to_ntt, int mont, cudaStream_t st) {
   if (B <= 0) return 0;
-  typedef Geo<LOGN, Loge32<LOGN>::v> G_;
-  auto kern = k_plain_to_rns<LOGN>;
-  if (int r = set_smem(kern, smem32<LOGN>())) return r;
-  dim3 grid(c->k, (unsigned)B);
-  kern<<<grid, G_::NT, smem32<LOGN>(), st>>>(poly, out, c->k, c->t, mode, to_ntt, mont, c->d_delta,
-                                             c->d_tw32, c->d_info32);
-  HEFV_LAUNCH_CHECK("k_plain_to_rns");
+  const int64_t total = B << LOGN;
+  k_plain_residues<<<grid_for(total, 256), 256, 0, st>>>(poly, out, B, c->k, LOGN, c->t, mode,
+                                                         c->d_delta, c->d_info32);
+  HEFV_LAUNCH_CHECK("k_plain_residues");
+  if (to_ntt)
+    if (int r = hefv_ntt_fwd32(c, out, out, B, c->k, 0, 0, st)) return r;
+  if (mont)
+    if (int r = hefv_to_montgomery(c, out, out, B, st)) return r;
   return 0;
 }
 

@@ -283,27 +283,34 @@ def planned_layer_eval(backend, rows, x, skip_zero_segments=True, scale_factor=1
     # depth checks up front (the serial schedule raises at the first offending cmult)
     budget = params.depth_budget
     row_level = np.zeros(R, dtype=np.int64)
-    for i in np.nonzero(has_acc)[0]:
-        lv = max(x_levels[int(sg)] for sg in seg_lists[i]) + 1
-        if lv > budget or lv + 1 > budget:
-            bad = lv if lv > budget else lv + 1
+    act = np.nonzero(has_acc)[0]
+    if len(act):
+        segs = np.concatenate([np.asarray(seg_lists[i], dtype=np.int64) for i in act])
+        starts = np.concatenate(([0], np.cumsum(nseg[act])[:-1]))
+        lv = np.maximum.reduceat(np.asarray(x_levels, dtype=np.int64)[segs], starts) + 1
+        over = np.nonzero(lv + 1 > budget)[0]  # the cmult (lv) or the e0 mask (lv + 1)
+        if len(over):
+            first = int(lv[over[0]])
+            bad = first if first > budget else first + 1
             raise DepthBudgetError(f"operation needs level {bad} but depth_budget is {budget}")
-        row_level[i] = lv
+        row_level[act] = lv
 
-    seen_m, plain_bias = replay_ledger(backend._c, rows, x_k=x.k, s=s, width=width,
-                                       n_iter=n_iter, m_arr=m_arr, off_arr=off_arr,
-                                       bias_arr=bias_arr, nseg=nseg, row_level=row_level)
-
-    # ---- device work ------------------------------------------------------------
-    active = np.nonzero(has_acc)[0]
+    # ---- device work (queued chunk by chunk; the host plans chunk c + 1 while
+    # the GPU runs chunk c) -----------------------------------------------------------
+    active = act
     out_dev = torch.zeros((nout, 2, kq, n), dtype=torch.int32, device="cuda")
-    out_level = [0] * nout
-    for i in active:
-        m = int(m_arr[i])
-        out_level[m] = max(out_level[m], int(row_level[i]) + 1)
+    out_level_arr = np.zeros(nout, dtype=np.int64)
+    np.maximum.at(out_level_arr, m_arr[active], row_level[active] + 1)
+    out_level = [int(v) for v in out_level_arr]
     if len(active):
         _run_rows(backend, rows, x, seg_lists, active, m_arr, off_arr, bias_arr, out_dev,
                   n_iter, skip_zero_segments)
+
+    # the ledger of the serial schedule (host accounting; the device work does
+    # not touch it, so replaying it after the launches keeps the event order)
+    seen_m, plain_bias = replay_ledger(backend._c, rows, x_k=x.k, s=s, width=width,
+                                       n_iter=n_iter, m_arr=m_arr, off_arr=off_arr,
+                                       bias_arr=bias_arr, nseg=nseg, row_level=row_level)
 
     # ---- outputs + the reference's final loop (inference.py:342-348) ----------
     from .fv import FvCiphertext
@@ -343,8 +350,12 @@ def _sparse_plan(rows, order, s: int, t: int) -> dict:
         val = np.mod(np.concatenate(raw).astype(np.int64), t).astype(np.uint64)
     ridx = np.repeat(np.arange(len(order), dtype=np.int64), lens)
     seg = pos // s
-    perm = np.lexsort((seg, ridx))  # stable: keeps position order inside a segment
-    pos, val, ridx, seg = pos[perm], val[perm], ridx[perm], seg[perm]
+    # group by (row, segment), position order kept inside a segment; compiled
+    # conv / fc rows list their positions ascending, so this is usually the
+    # identity and the sort is skipped
+    if len(seg) > 1 and not np.all((ridx[1:] > ridx[:-1]) | (seg[1:] >= seg[:-1])):
+        perm = np.lexsort((seg, ridx))  # stable
+        pos, val, ridx, seg = pos[perm], val[perm], ridx[perm], seg[perm]
     key = ridx * (int(seg.max()) + 1) + seg
     starts = np.flatnonzero(np.concatenate(([True], key[1:] != key[:-1])))
     ptr = np.concatenate((starts, [len(key)])).astype(np.int64)
@@ -365,23 +376,40 @@ def _tile_rows(backend, n_plain_per_row: float) -> int:
 
 def _run_rows(backend, rows, x, seg_lists, active, m_arr, off_arr, bias_arr, out_dev, n_iter,
               skip_zero_segments):
-    """The device work of a layer: one hefv_layer_rows call (layer.cu) over
-    the active rows, grouped by output ciphertext.  Python only builds the
+    """The device work of a layer: hefv_layer_rows calls (layer.cu) over the
+    active rows, grouped by output ciphertext, in chunks so that the host
+    plans chunk c + 1 while the GPU runs chunk c.  Python only builds the
     host plan (CSR plaintexts, per-row output / offset / bias) and the
     workspaces; tiling, AllSum, biases, the e0 mask, placement hops and the
     output sums run in C++."""
+    import torch
+
+    ctx = backend.ctx
+    s = x.slots_used
+    xin = torch.stack([backend.dev(ct)[:2] for ct in x.cts]).contiguous()
+    order = active[np.argsort(m_arr[active], kind="stable")]
+    avg_plain = max(1.0, float(np.mean([len(seg_lists[i]) for i in order])))
+    T = _tile_rows(backend, avg_plain)
+    # one tile first (its planning is the only host time the GPU waits for),
+    # then growing chunks planned while the previous ones run
+    lo, size = 0, T
+    while lo < len(order):
+        _layer_rows_call(backend, rows, xin, len(x.cts), order[lo:lo + size], m_arr, off_arr,
+                         bias_arr, out_dev, n_iter, s, T)
+        lo += size
+        size = min(8 * T, 2 * size)
+
+
+def _layer_rows_call(backend, rows, xin, x_cts, order, m_arr, off_arr, bias_arr, out_dev, n_iter,
+                     s, T):
+    """One hefv_layer_rows call over the rows ``order`` (grouped by output)."""
     import ctypes as C
 
     import torch
 
     ctx = backend.ctx
-    s = x.slots_used
     t = backend.params.plain_modulus
-    xin = torch.stack([backend.dev(ct)[:2] for ct in x.cts]).contiguous()
-    order = active[np.argsort(m_arr[active], kind="stable")]
     R = len(order)
-    avg_plain = max(1.0, float(np.mean([len(seg_lists[i]) for i in order])))
-    T = _tile_rows(backend, avg_plain)
     plan = _sparse_plan(rows, order, s, t)
     row_out = np.ascontiguousarray(m_arr[order], dtype=np.int32)
     row_off = np.ascontiguousarray(off_arr[order], dtype=np.int32)
@@ -399,7 +427,7 @@ def _run_rows(backend, rows, x, seg_lists, active, m_arr, off_arr, bias_arr, out
         return a.ctypes.data if a.size else None
 
     words = C.c_int64()
-    ctx.call("hefv_layer_rows_work_words", len(x.cts), R, ptr(row_ptr), T, C.byref(words))
+    ctx.call("hefv_layer_rows_work_words", x_cts, R, ptr(row_ptr), T, C.byref(words))
     work = torch.empty(words.value, dtype=torch.int32, device="cuda")
     if ctx.ks_aux:
         ws, cap = _ks_workspace(ctx, T)
@@ -408,7 +436,7 @@ def _run_rows(backend, rows, x, seg_lists, active, m_arr, off_arr, bias_arr, out
         ws_ptr, cap = None, 0
     h2d0 = C.c_int64()
     ctx.call("hefv_transfer_stats", C.byref(h2d0), None)
-    ctx.call("hefv_layer_rows", xin.data_ptr(), len(x.cts), R, ptr(row_out), ptr(row_off),
+    ctx.call("hefv_layer_rows", xin.data_ptr(), x_cts, R, ptr(row_out), ptr(row_off),
              ptr(row_bias), ptr(row_ptr), ptr(plain_seg), ptr(plain_ptr), ptr(slot_idx),
              ptr(slot_val), n_iter, backend.params.slot_count, len(offsets), ptr(offsets),
              handles, out_dev.data_ptr(), out_dev.shape[0], T, work.data_ptr(), words.value,
