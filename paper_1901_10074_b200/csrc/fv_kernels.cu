@@ -66,6 +66,11 @@ static int set_smem(K kern, size_t bytes) {
   return 0;
 }
 
+// a * b * 2^-32 mod p, canonical (b in Montgomery form gives a * b_plain)
+__device__ __forceinline__ uint32_t mulmod_mont_canon(uint32_t a, uint32_t b, const Prime32Info& inf) {
+  const uint32_t r = mont_mul_lazy(a, b, inf.p, inf.pinv_neg);
+  return r >= inf.p ? r - inf.p : r;
+}
 __device__ __forceinline__ uint32_t mulmod_small(uint32_t a, uint32_t b, const Prime32Info& inf) {
   return barrett62((uint64_t)a * b, inf.p, inf.mu);
 }
@@ -470,86 +475,83 @@ static int run_decrypt_acc(hefv_ctx* c, const uint32_t* ct, int nparts, const ui
 // ---------------------------------------------------------------------------
 // ciphertext x plaintext (fv.py:364-375) and the planner's row MAC
 // ---------------------------------------------------------------------------
-template <int LOGN>
-__global__ void __launch_bounds__(Geo<LOGN, Loge32<LOGN>::v>::NT)
-    k_mul_plain(const uint32_t* __restrict__ ct, const uint32_t* __restrict__ m_ntt,
-                uint32_t* __restrict__ out, int nparts, int k, int m_broadcast,
-                const uint2* __restrict__ tw_all, const uint2* __restrict__ itw_all,
-                const Prime32Info* __restrict__ info) {
-  constexpr int LE = Loge32<LOGN>::v;
-  typedef Geo<LOGN, LE> G_;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  uint32_t* sm = reinterpret_cast<uint32_t*>(smraw);
-  const int j = blockIdx.x;
-  const int part = blockIdx.y;
-  const size_t b = blockIdx.z;
-  const Prime32Info inf = info[j];
-  const Mod32 md = make_mod(inf);
-  const int tid = threadIdx.x;
-  const size_t N = G_::N;
-  const size_t off = ((b * nparts + part) * k + j) * N;
-  uint32_t x[G_::E];
+// ct x pt products and the planner's row MAC, in the NTT domain: an
+// elementwise Montgomery product (inputs NTT'd by the persistent batched
+// transform k_ntt32_b, twiddles staged in shared memory) and the batched
+// inverse transform, in place.  (A CTA per (prime, part, row) doing its own
+// transforms with L2-resident twiddles ran at a third of that rate.)
+__global__ void k_pointwise_mont(uint32_t* __restrict__ data, const uint32_t* __restrict__ m_ntt,
+                                 int64_t stacks, int nparts, int k, int log_n, int m_broadcast,
+                                 const Prime32Info* __restrict__ info) {
+  // data: (B, nparts, k, N) NTT values; m_ntt: (B or 1, k, N) Montgomery form
+  const int64_t n4 = (1ll << log_n) >> 2;
+  const int64_t total = stacks * k * n4;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = g / n4, q = g - row * n4;  // row = (b * nparts + part) * k + j
+    const int j = (int)(row % k);
+    const int64_t b = row / ((int64_t)k * nparts);
+    const Prime32Info inf = info[j];
+    uint4* d = reinterpret_cast<uint4*>(data) + g;
+    const uint4 m = reinterpret_cast<const uint4*>(m_ntt)[((m_broadcast ? 0 : b) * k + j) * n4 + q];
+    uint4 v = *d;
+    v.x = mulmod_mont_canon(v.x, m.x, inf);
+    v.y = mulmod_mont_canon(v.y, m.y, inf);
+    v.z = mulmod_mont_canon(v.z, m.z, inf);
+    v.w = mulmod_mont_canon(v.w, m.w, inf);
+    *d = v;
+  }
+}
+
+__global__ void k_rows_mac_ntt(const uint32_t* __restrict__ x_ntt, const uint32_t* __restrict__ m_ntt,
+                               const int32_t* __restrict__ row_ptr,
+                               const int32_t* __restrict__ plain_seg,
+                               const int32_t* __restrict__ plain_idx, uint32_t* __restrict__ out,
+                               int64_t R, int k, int log_n, const Prime32Info* __restrict__ info) {
+  // out (R, 2, k, N): row r, part, prime j, word i = sum over the row's
+  // plaintexts p of x_ntt[seg p][part][j][i] * m_ntt[p][j][i] (x Montgomery)
+  const int64_t n4 = (1ll << log_n) >> 2;
+  const int64_t total = R * k * n4;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rj = g / n4, q = g - rj * n4;
+    const int64_t r = rj / k;
+    const int j = (int)(rj - r * k);
+    const Prime32Info inf = info[j];
+    const Mod32 md = make_mod(inf);
+    uint32_t a0[4] = {0u, 0u, 0u, 0u}, a1[4] = {0u, 0u, 0u, 0u};
+    for (int p = row_ptr[r]; p < row_ptr[r + 1]; ++p) {
+      const int64_t seg = plain_seg[p];
+      const int64_t mi = plain_idx != nullptr ? plain_idx[p] : p;
+      const uint4 m = reinterpret_cast<const uint4*>(m_ntt)[(mi * k + j) * n4 + q];
+      const uint4 x0 = reinterpret_cast<const uint4*>(x_ntt)[((seg * 2) * k + j) * n4 + q];
+      const uint4 x1 = reinterpret_cast<const uint4*>(x_ntt)[((seg * 2 + 1) * k + j) * n4 + q];
+      const uint32_t mv[4] = {m.x, m.y, m.z, m.w};
+      const uint32_t xv0[4] = {x0.x, x0.y, x0.z, x0.w}, xv1[4] = {x1.x, x1.y, x1.z, x1.w};
 #pragma unroll
-  for (int e = 0; e < G_::E; ++e) x[e] = ct[off + tid + e * G_::NT];
-  cta_fwd<LOGN, LE, Mod32>(md, x, sm, tw_all + (size_t)j * N);
-  const uint32_t* mm = m_ntt + ((m_broadcast ? 0 : b) * k + j) * N;
-#pragma unroll
-  for (int e = 0; e < G_::E; ++e) x[e] = mont_mul_lazy(x[e], mm[row_index<LOGN, LE>(tid, e)], inf.p, inf.pinv_neg);
-  __syncthreads();
-  cta_inv<LOGN, LE, Mod32>(md, x, sm, itw_all + (size_t)j * N, inf.ninv, inf.wn);
-#pragma unroll
-  for (int e = 0; e < G_::E; ++e) out[off + tid + e * G_::NT] = md.subp(x[e]);
+      for (int e = 0; e < 4; ++e) {
+        a0[e] = md.sub2p(a0[e] + mont_mul_lazy(mv[e], xv0[e], inf.p, inf.pinv_neg));
+        a1[e] = md.sub2p(a1[e] + mont_mul_lazy(mv[e], xv1[e], inf.p, inf.pinv_neg));
+      }
+    }
+    uint4* o = reinterpret_cast<uint4*>(out);
+    o[((r * 2) * k + j) * n4 + q] = make_uint4(md.subp(a0[0]), md.subp(a0[1]), md.subp(a0[2]),
+                                               md.subp(a0[3]));
+    o[((r * 2 + 1) * k + j) * n4 + q] = make_uint4(md.subp(a1[0]), md.subp(a1[1]),
+                                                   md.subp(a1[2]), md.subp(a1[3]));
+  }
 }
 
 template <int LOGN>
 static int run_mul_plain(hefv_ctx* c, const uint32_t* ct, const uint32_t* m, uint32_t* out,
                          int64_t B, int nparts, int bc, cudaStream_t st) {
   if (B <= 0) return 0;
-  if (B > 65535) return fail("mul_plain: batch > 65535");
-  typedef Geo<LOGN, Loge32<LOGN>::v> G_;
-  auto kern = k_mul_plain<LOGN>;
-  if (int r = set_smem(kern, smem32<LOGN>())) return r;
-  dim3 grid(c->k, nparts, (unsigned)B);
-  kern<<<grid, G_::NT, smem32<LOGN>(), st>>>(ct, m, out, nparts, c->k, bc, c->d_tw32, c->d_itw32,
-                                             c->d_info32);
-  HEFV_LAUNCH_CHECK("k_mul_plain");
-  return 0;
-}
-
-template <int LOGN>
-__global__ void __launch_bounds__(Geo<LOGN, Loge32<LOGN>::v>::NT)
-    k_rows_mac(const uint32_t* __restrict__ x_ntt, const uint32_t* __restrict__ m_ntt,
-               const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ plain_seg,
-               const int32_t* __restrict__ plain_idx, uint32_t* __restrict__ out, int k,
-               const uint2* __restrict__ itw_all, const Prime32Info* __restrict__ info) {
-  constexpr int LE = Loge32<LOGN>::v;
-  typedef Geo<LOGN, LE> G_;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  uint32_t* sm = reinterpret_cast<uint32_t*>(smraw);
-  const int j = blockIdx.x;
-  const int part = blockIdx.y;
-  const size_t r = blockIdx.z;
-  const Prime32Info inf = info[j];
-  const Mod32 md = make_mod(inf);
-  const int tid = threadIdx.x;
-  const size_t N = G_::N;
-  uint32_t acc[G_::E];
-#pragma unroll
-  for (int e = 0; e < G_::E; ++e) acc[e] = 0;
-  const int lo = row_ptr[r], hi = row_ptr[r + 1];
-  for (int p = lo; p < hi; ++p) {
-    const int seg = plain_seg[p];
-    const uint32_t* xs = x_ntt + (((size_t)seg * 2 + part) * k + j) * N;
-    const size_t mi = plain_idx != nullptr ? (size_t)plain_idx[p] : (size_t)p;
-    const uint32_t* ms = m_ntt + (mi * k + j) * N;
-#pragma unroll
-    for (int e = 0; e < G_::E; ++e)
-      acc[e] = md.sub2p(acc[e] + mont_mul_lazy(ms[row_index<LOGN, LE>(tid, e)], xs[row_index<LOGN, LE>(tid, e)], inf.p, inf.pinv_neg));
-  }
-  cta_inv<LOGN, LE, Mod32>(md, acc, sm, itw_all + (size_t)j * N, inf.ninv, inf.wn);
-  uint32_t* dst = out + ((r * 2 + part) * k + j) * N;
-#pragma unroll
-  for (int e = 0; e < G_::E; ++e) dst[tid + e * G_::NT] = md.subp(acc[e]);
+  const int64_t stacks = B * nparts;
+  if (int r = hefv_ntt_fwd32(c, ct, out, stacks, c->k, 0, 0, st)) return r;
+  k_pointwise_mont<<<grid_for(stacks * c->k * ((int64_t)1 << LOGN) / 4, 256), 256, 0, st>>>(
+      out, m, stacks, nparts, c->k, LOGN, bc, c->d_info32);
+  HEFV_LAUNCH_CHECK("k_pointwise_mont");
+  return hefv_ntt_inv32(c, out, out, stacks, c->k, 0, 0, st);
 }
 
 template <int LOGN>
@@ -557,15 +559,10 @@ static int run_rows_mac(hefv_ctx* c, const uint32_t* x, const uint32_t* m, const
                         const int32_t* seg, const int32_t* pidx, uint32_t* out, int64_t R,
                         cudaStream_t st) {
   if (R <= 0) return 0;
-  if (R > 65535) return fail("rows_mac: more than 65535 rows per call");
-  typedef Geo<LOGN, Loge32<LOGN>::v> G_;
-  auto kern = k_rows_mac<LOGN>;
-  if (int r = set_smem(kern, smem32<LOGN>())) return r;
-  dim3 grid(c->k, 2, (unsigned)R);
-  kern<<<grid, G_::NT, smem32<LOGN>(), st>>>(x, m, rp, seg, pidx, out, c->k, c->d_itw32,
-                                             c->d_info32);
-  HEFV_LAUNCH_CHECK("k_rows_mac");
-  return 0;
+  k_rows_mac_ntt<<<grid_for(R * c->k * ((int64_t)1 << LOGN) / 4, 256), 256, 0, st>>>(
+      x, m, rp, seg, pidx, out, R, c->k, LOGN, c->d_info32);
+  HEFV_LAUNCH_CHECK("k_rows_mac_ntt");
+  return hefv_ntt_inv32(c, out, out, 2 * R, c->k, 0, 0, st);
 }
 
 // ---------------------------------------------------------------------------
