@@ -218,7 +218,7 @@ int hefv_add_part0(hefv_ctx* ctx, uint32_t* rows, int64_t row_stride, const int3
  *   8 k N max(q_j)^2 < a_0 a_1 a_2 and k a_t^2 < 2^62 (k <= 24).
  * hefv_ks_aux_key: switch key (k, k, N) Montgomery device order (as for
  *   hefv_keyswitch) -> kaux (3, 2k, k, N) = NTT_{a_t}(iNTT_j(K_ji)), parts
- *   [body j | mask j].
+ *   [body j | mask j]; hefv_ks_aux_key_words gives its size in words.
  * hefv_keyswitch_aux: arguments as hefv_keyswitch, plus
  *   dig_slot: item b's digit rows come from digits + dig_slot[b] * dig_stride
  *     (NULL: b * dig_stride);
@@ -229,6 +229,7 @@ int hefv_add_part0(hefv_ctx* ctx, uint32_t* rows, int64_t row_stride, const int3
 int hefv_ks_aux_setup(hefv_ctx* ctx, int32_t aux_base);
 int hefv_ks_aux_key(hefv_ctx* ctx, const uint32_t* kbody, const uint32_t* kmask, uint32_t* kaux,
                     void* stream);
+int hefv_ks_aux_key_words(hefv_ctx* ctx, int64_t* words);
 int hefv_keyswitch_aux(hefv_ctx* ctx, const uint32_t* kaux, const uint32_t* digits,
                        int64_t dig_stride, const int32_t* dig_slot, uint32_t galois_elt,
                        uint32_t* out0, uint32_t* out1, int64_t out_stride,
@@ -369,6 +370,12 @@ int hefv_transfer_stats(hefv_ctx* ctx, int64_t* h2d, int64_t* d2h);
  * function): kind 0 IMAD, 1 IMAD.HI, 2 IMAD.WIDE, 3 IADD3, 4 Shoup butterfly;
  * executes blocks * 256 * iters * 128 operations. */
 int hefv_probe_int(int32_t kind, int32_t blocks, int32_t iters, uint32_t* out, void* stream);
+/* tcgen05 int8 check: C (128 x 256 s32) = A (128 x 32ks u8) x B (256 x 32ks u8)^T. */
+int hefv_probe_umma(const uint8_t* A, const uint8_t* B, int32_t* C, int32_t ks, void* stream);
+/* TMEM load-shape check (development aid): out[t * 4 + r] = register r of thread t. */
+int hefv_probe_tmem_shape(int32_t* out, int32_t shape, void* stream);
+/* tcgen05 MMA latency / throughput (development aid). */
+int hefv_probe_umma_lat(int64_t* out, int32_t reps, int32_t chain, int32_t depth, void* stream);
 
 #ifdef __cplusplus
 }

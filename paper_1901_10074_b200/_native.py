@@ -47,6 +47,7 @@ _SIGS = {
     "hefv_keyswitch": [_P, _P, _P, _P, _I64, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _I64, _I64, _P],
     "hefv_ks_aux_setup": [_P, _I32],
     "hefv_ks_aux_key": [_P, _P, _P, _P, _P],
+    "hefv_ks_aux_key_words": [_P, _P],
     "hefv_keyswitch_aux": [_P, _P, _P, _I64, _P, _U32, _P, _P, _I64, _P, _P, _P, _I64, _P, _P,
                            _I64, _P, _I64, _I64, _P],
     "hefv_keygen_digit": [_P, _P, _P, _I32, _P, _P, _P, _P, _P, _P],
@@ -56,6 +57,9 @@ _SIGS = {
     "hefv_add_part0": [_P, _P, _I64, _P, _P, _I64, _P],
     "hefv_rows_mac_indexed": [_P, _P, _P, _P, _P, _P, _P, _I64, _P],
     "hefv_probe_int": [_I32, _I32, _I32, _P, _P],
+    "hefv_probe_umma": [_P, _P, _P, _I32, _P],
+    "hefv_probe_tmem_shape": [_P, _I32, _P],
+    "hefv_probe_umma_lat": [_P, _I32, _I32, _I32, _P],
     "hefv_keyswitch64": [_P, _P, _P, _P, _P, _P, _I64, _P],
     "hefv_to_montgomery64": [_P, _P, _P, _I64, _P],
     "hefv_ks64_aux_setup": [_P, _I32],

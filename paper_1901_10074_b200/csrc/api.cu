@@ -206,7 +206,9 @@ int hefv_key_upload(hefv_ctx* c, const int64_t* body, const int64_t* mask, hefv_
     if (cudaGetLastError() != cudaSuccess) return cleanup(fail("hefv_key_upload: launch failed"));
   }
   if (c->ksa_ready) {
-    if (cudaMalloc(reinterpret_cast<void**>(&key->aux), 6 * words * 4) != cudaSuccess)
+    int64_t aux_words = 0;
+    if (int r = hefv_ks_aux_key_words(c, &aux_words)) return cleanup(r);
+    if (cudaMalloc(reinterpret_cast<void**>(&key->aux), (size_t)aux_words * 4) != cudaSuccess)
       return cleanup(fail("hefv_key_upload: out of device memory (aux key)"));
     if (int r = hefv_ks_aux_key(c, key->body, key->mask, key->aux, st)) return cleanup(r);
   }

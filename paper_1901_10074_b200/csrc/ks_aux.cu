@@ -858,6 +858,13 @@ int hefv_ks_aux_key(hefv_ctx* c, const uint32_t* kbody, const uint32_t* kmask, u
   HEFV_KSA_DISPATCH(run_ksa_key, c, kbody, kmask, kaux, st)
 }
 
+int hefv_ks_aux_key_words(hefv_ctx* c, int64_t* words) {
+  if (!c || !c->ksa_ready) return fail("hefv_ks_aux_key_words: aux key switch not set up");
+  if (!words) return fail("hefv_ks_aux_key_words: null pointer");
+  *words = (int64_t)6 * c->k * c->k * c->n;  // (3, 2k, k, N)
+  return 0;
+}
+
 int hefv_keyswitch_aux(hefv_ctx* c, const uint32_t* kaux, const uint32_t* digits,
                        int64_t dig_stride, const int32_t* dig_slot, uint32_t galois_elt,
                        uint32_t* out0, uint32_t* out1, int64_t out_stride,

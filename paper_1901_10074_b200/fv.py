@@ -298,12 +298,16 @@ class SwitchKey:
         self._ctx = ctx
         self.body_dev = body_dev
         self.mask_dev = mask_dev
-        # aux-basis form for hefv_keyswitch_aux: (3, 2k, k, N)
+        # aux-basis form for hefv_keyswitch_aux (the tensor-core contraction's
+        # per-point key operands; hefv_ks_aux_key_words)
         self.aux_dev = None
         if ctx.ks_aux:
+            import ctypes as C
+
             torch = _torch()
-            self.aux_dev = torch.empty((3, 2 * ctx.k, ctx.k, ctx.n), dtype=torch.int32,
-                                       device="cuda")
+            words = C.c_int64()
+            ctx.call("hefv_ks_aux_key_words", C.byref(words))
+            self.aux_dev = torch.empty(words.value, dtype=torch.int32, device="cuda")
             ctx.call("hefv_ks_aux_key", body_dev.data_ptr(), mask_dev.data_ptr(),
                      self.aux_dev.data_ptr(), ctx.stream())
         self._handle = None
