@@ -193,3 +193,57 @@ def test_c_host_program(pair, tmp_path):
     for i, want in enumerate(wants):
         assert np.array_equal(got[i], _stack(want.parts)), ["rotate", "mult", "add", "add_plain",
                                                              "cmult"][i]
+
+
+def test_layer_rows_rejects_bad_plans(pair):
+    """hefv_layer_rows validates the host plan before any launch."""
+    import torch
+
+    from paper_1901_10074_b200.errors import NativeError
+
+    gpu, _ = pair
+    ctx = gpu.ctx
+    st = ctx.stream()
+    k, n = ctx.k, ctx.n
+    x = torch.zeros((1, 2, k, n), dtype=torch.int32, device="cuda")
+    out = torch.zeros((2, 2, k, n), dtype=torch.int32, device="cuda")
+    galois = gpu.keys.galois
+    offs = np.array(sorted(galois), dtype=np.int32)
+    handles = (C.c_void_p * len(offs))(*[galois[int(o)].handle.value for o in offs])
+
+    def call(row_out, plain_seg, n_iter=1, work_words=None, slot=0, key_offs=offs):
+        R = len(row_out)
+        row_out = np.asarray(row_out, dtype=np.int32)
+        row_off = np.zeros(R, dtype=np.int32)
+        row_ptr = np.arange(R + 1, dtype=np.int64)
+        plain_seg = np.asarray(plain_seg, dtype=np.int32)
+        plain_ptr = np.arange(R + 1, dtype=np.int64)
+        slot_idx = np.full(R, slot, dtype=np.int32)
+        slot_val = np.ones(R, dtype=np.uint64)
+        words = C.c_int64()
+        ctx.call("hefv_layer_rows_work_words", 1, R, row_ptr.ctypes.data, 4, C.byref(words))
+        work = torch.empty(words.value, dtype=torch.int32, device="cuda")
+        ww = words.value if work_words is None else work_words
+        ws, cap = (None, 0)
+        if ctx.ks_aux:
+            from paper_1901_10074_b200.planner import _ks_workspace
+
+            wst, cap = _ks_workspace(ctx, 4)
+            ws = wst.data_ptr()
+        ctx.call("hefv_layer_rows", x.data_ptr(), 1, R, row_out.ctypes.data, row_off.ctypes.data,
+                 None, row_ptr.ctypes.data, plain_seg.ctypes.data, plain_ptr.ctypes.data,
+                 slot_idx.ctypes.data, slot_val.ctypes.data, n_iter, gpu.params.slot_count,
+                 len(key_offs), key_offs.ctypes.data, handles, out.data_ptr(), 2, 4,
+                 work.data_ptr(), ww, ws, cap, st)
+
+    call([0, 1], [0, 0])  # a valid two-row plan runs
+    with pytest.raises(NativeError, match="grouped by output"):
+        call([1, 0], [0, 0])
+    with pytest.raises(NativeError, match="segment outside"):
+        call([0, 1], [0, 3])
+    with pytest.raises(NativeError, match="workspace too small"):
+        call([0, 1], [0, 0], work_words=16)
+    with pytest.raises(NativeError, match="outside \\[0, N/2\\)"):
+        call([0, 1], [0, 0], slot=n)
+    with pytest.raises(NativeError, match="power-of-two Galois key"):
+        call([0, 1], [0, 0], n_iter=12, key_offs=offs[:1])
