@@ -262,11 +262,13 @@ void hefv_ctx_destroy(hefv_ctx* c) {
   cudaFree(c->d_ks64a_t);
   cudaFree(c->d_ks64a_j);
   drop_ks_events(c);
-  if (c->stage_done) {
-    cudaEventSynchronize(c->stage_done);
-    cudaEventDestroy(c->stage_done);
+  for (auto& sg : c->stages) {
+    if (sg.done) {
+      cudaEventSynchronize(sg.done);
+      cudaEventDestroy(sg.done);
+    }
+    if (sg.host) cudaFreeHost(sg.host);
   }
-  if (c->h_stage) cudaFreeHost(c->h_stage);
   delete c;
 }
 

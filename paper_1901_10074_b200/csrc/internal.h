@@ -78,10 +78,16 @@ struct hefv_ctx {
   std::vector<cudaEvent_t> ks_events;  // (begin, end) pairs
   // host -> device bytes copied by the library itself (plans, uploads)
   int64_t h2d_bytes = 0, d2h_bytes = 0;
-  // pinned staging of the layer planner's host plan (hefv_layer_rows)
-  void* h_stage = nullptr;
-  size_t h_stage_bytes = 0;
-  cudaEvent_t stage_done = nullptr;
+  // pinned staging buffers of the layer planner's host plans
+  // (hefv_layer_rows): a buffer is reused once the copy recorded by its
+  // event has completed, so calls on several streams never wait for each
+  // other's queued work
+  struct Stage {
+    void* host = nullptr;
+    size_t bytes = 0;
+    cudaEvent_t done = nullptr;
+  };
+  std::vector<Stage> stages;
 };
 
 // switch-key handle of the object-level C-ABI (api.cu)

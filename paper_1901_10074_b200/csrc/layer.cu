@@ -16,7 +16,8 @@
 //   5. per-output-ciphertext sums of the pieces.
 // The host part is only bookkeeping: the plan (CSR plaintexts, per-tile hop
 // groups and output segments) is built once per call in a pinned staging
-// buffer and copied to the device in one transfer.
+// buffer (a per-context pool: a buffer is reused once its copy is done) and
+// copied to the device in one transfer.
 #include <algorithm>
 #include <cstring>
 #include <map>
@@ -251,16 +252,23 @@ int hefv_layer_rows(hefv_ctx* c, const uint32_t* x, int32_t x_cts, int64_t R,
 
   // ---- one pinned transfer of the plan
   const size_t plan_bytes = sg.bytes.size();
-  if (c->stage_done) HEFV_CUDA(cudaEventSynchronize(c->stage_done));  // previous plan copied
-  if (c->h_stage_bytes < plan_bytes) {
-    if (c->h_stage) cudaFreeHost(c->h_stage);
-    c->h_stage = nullptr;
-    c->h_stage_bytes = 0;
-    HEFV_CUDA(cudaMallocHost(&c->h_stage, plan_bytes));
-    c->h_stage_bytes = plan_bytes;
+  // a pinned buffer whose last copy has completed (or a new one)
+  hefv_ctx::Stage* stage = nullptr;
+  for (auto& cand : c->stages)
+    if (cudaEventQuery(cand.done) == cudaSuccess && (!stage || cand.bytes > stage->bytes)) stage = &cand;
+  if (!stage) {
+    c->stages.emplace_back();
+    stage = &c->stages.back();
+    HEFV_CUDA(cudaEventCreateWithFlags(&stage->done, cudaEventDisableTiming));
   }
-  if (!c->stage_done) HEFV_CUDA(cudaEventCreateWithFlags(&c->stage_done, cudaEventDisableTiming));
-  std::memcpy(c->h_stage, sg.bytes.data(), plan_bytes);
+  if (stage->bytes < plan_bytes) {
+    if (stage->host) cudaFreeHost(stage->host);
+    stage->host = nullptr;
+    stage->bytes = 0;
+    HEFV_CUDA(cudaMallocHost(&stage->host, plan_bytes));
+    stage->bytes = plan_bytes;
+  }
+  std::memcpy(stage->host, sg.bytes.data(), plan_bytes);
   unsigned char* d_plan = nullptr;
   HEFV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_plan), plan_bytes, st));
   struct PlanFree {
@@ -268,9 +276,9 @@ int hefv_layer_rows(hefv_ctx* c, const uint32_t* x, int32_t x_cts, int64_t R,
     cudaStream_t st;
     ~PlanFree() { cudaFreeAsync(p, st); }
   } plan_free{d_plan, st};
-  HEFV_CUDA(cudaMemcpyAsync(d_plan, c->h_stage, plan_bytes, cudaMemcpyHostToDevice, st));
+  HEFV_CUDA(cudaMemcpyAsync(d_plan, stage->host, plan_bytes, cudaMemcpyHostToDevice, st));
   c->h2d_bytes += (int64_t)plan_bytes;
-  HEFV_CUDA(cudaEventRecord(c->stage_done, st));
+  HEFV_CUDA(cudaEventRecord(stage->done, st));
   auto P32 = [&](size_t off) { return reinterpret_cast<int32_t*>(d_plan + off); };
   auto P64 = [&](size_t off) { return reinterpret_cast<uint64_t*>(d_plan + off); };
 

@@ -117,25 +117,30 @@ def _budget(limit: int, held: int = 0) -> int:
 
 def _ks_workspace(ctx, batch: int):
     """Scratch of the aux-basis key switch (9 k N words per ciphertext),
-    cached on the context (``release_workspace`` drops it); ciphertexts
-    beyond its capacity run in chunks.  Sized from KS_WORKSPACE_BYTES and
-    the free device memory, so several live contexts do not each pin 24 GB."""
+    cached on the context per CUDA stream (work queued on two streams must
+    not share it; ``release_workspace`` drops them); ciphertexts beyond its
+    capacity run in chunks.  Sized from KS_WORKSPACE_BYTES and the free
+    device memory, so several live contexts do not each pin 24 GB."""
     import torch
 
     per_ct = 9 * ctx.k * ctx.n
-    ws = getattr(ctx, "_ks_ws", None)
+    cache = getattr(ctx, "_ks_ws", None)
+    if cache is None:
+        cache = ctx._ks_ws = {}
+    key = torch.cuda.current_stream().cuda_stream
+    ws = cache.get(key)
     held = 0 if ws is None else ws.numel() * 4
     if ws is not None and ws.numel() >= min(batch, KS_WORKSPACE_BYTES // (4 * per_ct)) * per_ct:
         return ws, ws.numel() // per_ct
     cap = max(1, min(batch, _budget(KS_WORKSPACE_BYTES, held) // (4 * per_ct)))
     if ws is None or ws.numel() < cap * per_ct:
-        ws = ctx._ks_ws = None      # the old buffer is freed before the new one is allocated
-        ws = ctx._ks_ws = torch.empty(cap * per_ct, dtype=torch.int32, device="cuda")
+        cache[key] = ws = None      # the old buffer is freed before the new one is allocated
+        cache[key] = ws = torch.empty(cap * per_ct, dtype=torch.int32, device="cuda")
     return ws, ws.numel() // per_ct
 
 
 def release_workspace(ctx) -> None:
-    """Drop the key-switch workspace cached on ``ctx``."""
+    """Drop the key-switch workspaces cached on ``ctx``."""
     ctx._ks_ws = None
 
 
