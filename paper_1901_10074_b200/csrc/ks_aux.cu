@@ -163,9 +163,11 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
       if (tid == 0 && nxt) bulk_g2s(stage, nxt, N * 4, mbar);
     };
     if constexpr (LASTSM) {
-      cta_fwd<LOGN, LOGE, Mod32, decltype(hook), false>(md, x, sm, tws, twg, hook);
-      const Mod32M mm{inf.p, 2 * inf.p, inf.pinv};
-      fwd_last_pass<LOGN, LOGE, Mod32M>(mm, x, tid, twl - NTW);
+      // 2^14: butterfly sums on the ALU pipe (Mod32A / Mod32MA, modarith.cuh)
+      const Mod32A ma(inf.p);
+      cta_fwd<LOGN, LOGE, Mod32A, decltype(hook), false>(ma, x, sm, tws, twg, hook);
+      const Mod32MA mm(inf.p, inf.pinv, ma.ones);
+      fwd_last_pass<LOGN, LOGE, Mod32MA>(mm, x, tid, twl - NTW);
     } else {
       cta_fwd<LOGN, LOGE, Mod32>(md, x, sm, tws, twg, hook, LOGN - G_::RLAST);
     }
@@ -183,6 +185,10 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
 #define KSA_STAGES_V 4
 #endif
 constexpr int KSA_STAGES = KSA_STAGES_V;  // depth of the digit-tile ring
+// Warps turning ring tiles into pair sums / interleaved pairs: two for the
+// 24-consumer CTA of k = 23, 24 (config-3 hop 24.4 -> 23.7 us), one otherwise
+// (two measured slower at k = 22: 20.7 -> 21.2 us).
+__host__ __device__ constexpr int ksa_pw(int JW) { return JW > 22 ? 2 : 1; }
 #ifndef KSA_MAC_ALLSMEM
 #define KSA_MAC_ALLSMEM 0  // k = 22 MAC: body key pairs in shared memory too (A/B)
 #endif
@@ -225,8 +231,9 @@ struct Redc {
 // K: digits per point (compile time, even; ring rows k..K-1 are zeroed once
 // and their key words are zero, so padded pairs contribute nothing).
 // Warps 0..JW-1 consume (warp w = target prime j = blockIdx.z * JW + w when
-// j < k), warp JW+1 streams each ciphertext's k x 32-word digit tile with one
-// bulk copy into a KSA_STAGES-deep ring, and warp JW turns every ring tile
+// j < k), the last warp streams each ciphertext's k x 32-word digit tile with one
+// bulk copy into a KSA_STAGES-deep ring, and warp JW (plus JW+1 when ksa_pw(JW)
+// is 2, taking alternate ciphertexts) turns every ring tile
 // into (a) the x-pair sums and (b) an interleaved copy xx[u][lane] =
 // (x_2u, x_2u+1), so a consumer loads each packed pair with one 64-bit
 // shared load.  Barriers (no CTA-wide barrier in the loop): full / empty
@@ -252,11 +259,12 @@ __device__ __forceinline__ void mba(uint32_t a) {
 }
 
 template <int K, int JW>
-__global__ void __launch_bounds__(32 * (JW + 2), 1)
+__global__ void __launch_bounds__(32 * (JW + 1 + ksa_pw(JW)), 1)
     k_ksa_mac(const uint32_t* __restrict__ X, const uint32_t* __restrict__ kaux,
               uint32_t* __restrict__ Y, int64_t B, int k, int log_n, int aux_base,
               const Prime32Info* __restrict__ info) {
   static_assert(K % 2 == 0, "digit pairs");
+  constexpr int KSA_PW = ksa_pw(JW);
   constexpr int H = K / 2;
   constexpr int S = KSA_STAGES;
   __shared__ __align__(128) uint32_t ring[S][K * 32];
@@ -286,7 +294,7 @@ __global__ void __launch_bounds__(32 * (JW + 2), 1)
   for (int q = k * 32 + threadIdx.x; q < K * 32; q += blockDim.x)
     for (int st = 0; st < S; ++st) ring[st][q] = 0u;
   __syncthreads();
-  if (w == JW + 1) {  // producer
+  if (w == JW + KSA_PW) {  // producer
     if (lane == 0) {
       const uint32_t tile_bytes = (uint32_t)k * 32 * 4;
       // X tile of ciphertext b: (((b * 3 + t) * tiles + m) * k) * 32 words, k*32 long
@@ -300,8 +308,9 @@ __global__ void __launch_bounds__(32 * (JW + 2), 1)
     }
     return;
   }
-  if (w == JW) {  // pair warp: x-pair sums + interleaved pairs
-    for (int r = 0; r < nb; ++r) {
+  if (w >= JW) {  // pair warps: x-pair sums + interleaved pairs (ciphertext r by warp r % KSA_PW)
+    static_assert(S % KSA_PW == 0, "a ring stage belongs to one pair warp");
+    for (int r = w - JW; r < nb; r += KSA_PW) {
       const int st = r % S;
       mbw(full0 + 8 * st, (uint32_t)((r / S) & 1));
       if (r >= S) mbw(xempty0 + 8 * st, (uint32_t)((r / S - 1) & 1));
@@ -696,19 +705,19 @@ static int run_ksa_e(hefv_ctx* c, const uint32_t* kaux, const uint32_t* dig, int
         HEFV_CUDA(cudaFuncSetAttribute(k_ksa_mac<22, 22>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)dyn(22, 22)));
-        k_ksa_mac<22, 22><<<grid, 32 * 24, dyn(22, 22), st>>>(X, kaux, Y, nb, k, c->log_n, ab,
+        k_ksa_mac<22, 22><<<grid, 32 * (23 + ksa_pw(22)), dyn(22, 22), st>>>(X, kaux, Y, nb, k, c->log_n, ab,
                                                                c->d_info32);
       } else if (k <= 16) {
-        k_ksa_mac<16, 16><<<grid, 32 * 18, 0, st>>>(X, kaux, Y, nb, k, c->log_n, ab, c->d_info32);
+        k_ksa_mac<16, 16><<<grid, 32 * (17 + ksa_pw(16)), 0, st>>>(X, kaux, Y, nb, k, c->log_n, ab, c->d_info32);
       } else if (k > 22) {
         HEFV_CUDA(cudaFuncSetAttribute(k_ksa_mac<24, 24>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)dyn(24, 24)));
-        k_ksa_mac<24, 24><<<grid, 32 * 26, dyn(24, 24), st>>>(X, kaux, Y, nb, k, c->log_n, ab,
+        k_ksa_mac<24, 24><<<grid, 32 * (25 + ksa_pw(24)), dyn(24, 24), st>>>(X, kaux, Y, nb, k, c->log_n, ab,
                                                                c->d_info32);
       } else {
         dim3 g2(grid.x, grid.y, (unsigned)((k + 11) / 12));
-        k_ksa_mac<KSA_KMAX, 12><<<g2, 32 * 14, 0, st>>>(X, kaux, Y, nb, k, c->log_n, ab,
+        k_ksa_mac<KSA_KMAX, 12><<<g2, 32 * (13 + ksa_pw(12)), 0, st>>>(X, kaux, Y, nb, k, c->log_n, ab,
                                                          c->d_info32);
       }
       HEFV_LAUNCH_CHECK("k_ksa_mac");

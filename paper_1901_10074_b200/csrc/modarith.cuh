@@ -21,6 +21,23 @@
 
 namespace hefv {
 
+// ptxas balances the FMA and ALU pipes by instruction COUNT and lowers plain
+// 32-bit adds to IMAD.IADD to do so; on sm_100a IMAD.HI / IMAD.WIDE issue at
+// half rate, so a forward butterfly loads the FMA pipe with 11 cycles against
+// the ALU's 8 (ncu, profiles/r02).  alu_add keeps an add on the ALU pipe:
+// min(a + b, 0xffffffff) with the constant opaque to the compiler is one
+// VIADDMNMX, which has no FMA-pipe form.  Measured (B200): 2^14 forward
+// +3.6 %; the inverse (-1.5 %) and the 2^12 forward (-2.4 %) lose, so only
+// the 2^14 forwards use the *A types below.
+__device__ __forceinline__ uint32_t opaque_ones() {
+  uint32_t v = 0xffffffffu;
+  asm volatile("" : "+r"(v));
+  return v;
+}
+__device__ __forceinline__ uint32_t alu_add(uint32_t a, uint32_t b, uint32_t ones) {
+  return min(a + b, ones);
+}
+
 // ---------------------------------------------------------------- 32-bit
 struct Mod32 {
   typedef uint32_t T;
@@ -89,6 +106,29 @@ struct Mod32M {
     uint32_t a = x, b = y;
     x = mul(a + b, ninv);
     y = mul(a - b + p2, wn);
+  }
+};
+
+// Forward-butterfly variants with the sum forced onto the ALU pipe (alu_add).
+struct Mod32A : Mod32 {
+  uint32_t ones;
+  __device__ __forceinline__ explicit Mod32A(uint32_t p_) : Mod32{p_, 2 * p_}, ones(opaque_ones()) {}
+  __device__ __forceinline__ void ct(uint32_t& x, uint32_t& y, Tw w) const {
+    uint32_t a = sub2p(x);
+    uint32_t t = mul_shoup(y, w.x, w.y, p);
+    x = alu_add(a, t, ones);
+    y = a - t + p2;
+  }
+};
+struct Mod32MA : Mod32M {
+  uint32_t ones;
+  __device__ __forceinline__ Mod32MA(uint32_t p_, uint32_t pinv_, uint32_t ones_)
+      : Mod32M{p_, 2 * p_, pinv_}, ones(ones_) {}
+  __device__ __forceinline__ void ct(uint32_t& x, uint32_t& y, Tw w) const {
+    uint32_t a = sub2p(x);
+    uint32_t t = mul(y, w);
+    x = alu_add(a, t, ones);
+    y = a - t + p2;
   }
 };
 

@@ -93,7 +93,8 @@ __device__ __forceinline__ void load_tw_run(const Tw* __restrict__ p, Tw* out, c
 
 template <int LOGN, int LOGE, class M>
 __device__ __forceinline__ void fwd_full_pass(const M& md, typename M::T* x, int pass, int tid,
-                                              const typename M::Tw* __restrict__ tw) {
+                                              const typename M::Tw* __restrict__ tw,
+                                              const int base = 1) {
   typedef Geo<LOGN, LOGE> G_;
   const int s0 = pass * LOGE;
   const int tsh = LOGN - s0 - LOGE;  // log2 of the element stride T
@@ -104,7 +105,7 @@ __device__ __forceinline__ void fwd_full_pass(const M& md, typename M::T* x, int
     if constexpr (sizeof(typename M::Tw) > 8) {
       // 64-bit primes: one 16-byte twiddle per butterfly group, loaded where
       // used (an array of 16-byte pairs would be placed in local memory)
-      const typename M::Tw* twb = tw + (1 << (s0 + l)) + (G << l);
+      const typename M::Tw* twb = tw + (base << (s0 + l)) + (G << l);
 #pragma unroll
       for (int u = 0; u < (1 << l); ++u) {
         const typename M::Tw wu = twb[u];
@@ -117,7 +118,7 @@ __device__ __forceinline__ void fwd_full_pass(const M& md, typename M::T* x, int
     } else {
       // the 2^l twiddles of this stage are contiguous: 16-byte loads
       typename M::Tw w[1 << (LOGE - 1)];
-      load_tw_run<typename M::Tw, (1 << (LOGE - 1))>(tw + (1 << (s0 + l)) + (G << l), w, 1 << l);
+      load_tw_run<typename M::Tw, (1 << (LOGE - 1))>(tw + (base << (s0 + l)) + (G << l), w, 1 << l);
 #pragma unroll
       for (int u = 0; u < (1 << l); ++u) {
 #pragma unroll
@@ -134,7 +135,7 @@ template <int LOGN, int LOGE, class M>
 __device__ __forceinline__ void fwd_last_pass(const M& md, typename M::T* x, int tid,
                                               const typename M::Tw* __restrict__ tw,
                                               const typename M::Tw* __restrict__ tw_hi = nullptr,
-                                              int split_log = 31) {
+                                              int split_log = 31, const int base = 1) {
   typedef Geo<LOGN, LOGE> G_;
   constexpr int R = G_::RLAST;
   constexpr int s0 = LOGN - R;
@@ -148,7 +149,7 @@ __device__ __forceinline__ void fwd_last_pass(const M& md, typename M::T* x, int
     // copy), the others `tw_hi` (global, through L1)
     const typename M::Tw* src = (tw_hi == nullptr || s0 + l + 1 <= split_log) ? tw : tw_hi;
     if constexpr (sizeof(typename M::Tw) > 8) {
-      const typename M::Tw* twb = src + (1 << (s0 + l)) + ((tid * BLK) << l);
+      const typename M::Tw* twb = src + (base << (s0 + l)) + ((tid * BLK) << l);
 #pragma unroll
       for (int b = 0; b < BLK; ++b) {
         typename M::T* xb = x + b * (1 << R);
@@ -164,7 +165,7 @@ __device__ __forceinline__ void fwd_last_pass(const M& md, typename M::T* x, int
       }
     } else {
       typename M::Tw w[BLK << (R - 1)];
-      load_tw_run<typename M::Tw, (BLK << (R - 1))>(src + (1 << (s0 + l)) + ((tid * BLK) << l),
+      load_tw_run<typename M::Tw, (BLK << (R - 1))>(src + (base << (s0 + l)) + ((tid * BLK) << l),
                                                     w, BLK << l);
 #pragma unroll
       for (int b = 0; b < BLK; ++b) {
@@ -271,13 +272,14 @@ template <int LOGN, int LOGE, class M, class Hook = NoHook, bool LAST = true>
 __device__ __forceinline__ void cta_fwd(const M& md, typename M::T* x, typename M::T* sm,
                                         const typename M::Tw* __restrict__ tw,
                                         const typename M::Tw* __restrict__ tw_last = nullptr,
-                                        const Hook& hook = Hook(), int split_log = 0) {
+                                        const Hook& hook = Hook(), int split_log = 0,
+                                        const int base = 1) {
   typedef Geo<LOGN, LOGE> G_;
   constexpr int LOG_NT = LOGN - LOGE;
   const int tid = threadIdx.x;
 #pragma unroll
   for (int pass = 0; pass < G_::NFULL; ++pass) {
-    fwd_full_pass<LOGN, LOGE, M>(md, x, pass, tid, tw);
+    fwd_full_pass<LOGN, LOGE, M>(md, x, pass, tid, tw, base);
     // pre-write barrier: CTA-wide before the first exchange (the tile may still
     // be read by the previous transform), group-wide afterwards
     if (pass == 0) {
@@ -302,17 +304,18 @@ __device__ __forceinline__ void cta_fwd(const M& md, typename M::T* x, typename 
   // (LAST = false: the caller runs it, e.g. with another twiddle form)
   if (!LAST) return;
   if (tw_last == nullptr)
-    fwd_last_pass<LOGN, LOGE, M>(md, x, tid, tw);
+    fwd_last_pass<LOGN, LOGE, M>(md, x, tid, tw, nullptr, 31, base);
   else
-    fwd_last_pass<LOGN, LOGE, M>(md, x, tid, tw, tw_last, split_log);
+    fwd_last_pass<LOGN, LOGE, M>(md, x, tid, tw, tw_last, split_log, base);
 }
 
 // ---- inverse (Gentleman-Sande, bit-reversed -> natural) -------------------
 
-template <int LOGN, int LOGE, class M>
+template <int LOGN, int LOGE, class M, bool SUB = false>
 __device__ __forceinline__ void inv_last_pass(const M& md, typename M::T* x, int tid,
                                               const typename M::Tw* __restrict__ itw,
-                                              const typename M::Tw& ninv, const typename M::Tw& wn) {
+                                              const typename M::Tw& ninv, const typename M::Tw& wn,
+                                              const int base = 1) {
   typedef Geo<LOGN, LOGE> G_;
   constexpr int R = G_::RLAST;
   constexpr int s0 = LOGN - R;
@@ -320,7 +323,7 @@ __device__ __forceinline__ void inv_last_pass(const M& md, typename M::T* x, int
 #pragma unroll
   for (int l = R - 1; l >= 0; --l) {
     const int half = (1 << R) >> (l + 1);
-    if (s0 + l == 0) {
+    if (s0 + l == 0 && !SUB) {
       // whole transform is one last pass (tiny N): merged N^-1 stage
 #pragma unroll
       for (int b = 0; b < BLK; ++b) {
@@ -331,7 +334,7 @@ __device__ __forceinline__ void inv_last_pass(const M& md, typename M::T* x, int
     }
     if constexpr (sizeof(typename M::Tw) > 8) {
       // 64-bit primes: twiddles loaded where used (see fwd_full_pass)
-      const typename M::Tw* twb = itw + (1 << (s0 + l)) + ((tid * BLK) << l);
+      const typename M::Tw* twb = itw + (base << (s0 + l)) + ((tid * BLK) << l);
 #pragma unroll
       for (int b = 0; b < BLK; ++b) {
         typename M::T* xb = x + b * (1 << R);
@@ -347,7 +350,7 @@ __device__ __forceinline__ void inv_last_pass(const M& md, typename M::T* x, int
       }
     } else {
       typename M::Tw w[BLK << (R - 1)];
-      load_tw_run<typename M::Tw, (BLK << (R - 1))>(itw + (1 << (s0 + l)) + ((tid * BLK) << l), w,
+      load_tw_run<typename M::Tw, (BLK << (R - 1))>(itw + (base << (s0 + l)) + ((tid * BLK) << l), w,
                                                     BLK << l);
 #pragma unroll
       for (int b = 0; b < BLK; ++b) {
@@ -365,10 +368,11 @@ __device__ __forceinline__ void inv_last_pass(const M& md, typename M::T* x, int
   }
 }
 
-template <int LOGN, int LOGE, class M>
+template <int LOGN, int LOGE, class M, bool SUB = false>
 __device__ __forceinline__ void inv_full_pass(const M& md, typename M::T* x, int pass, int tid,
                                               const typename M::Tw* __restrict__ itw,
-                                              const typename M::Tw& ninv, const typename M::Tw& wn) {
+                                              const typename M::Tw& ninv, const typename M::Tw& wn,
+                                              const int base = 1) {
   typedef Geo<LOGN, LOGE> G_;
   const int s0 = pass * LOGE;
   const int tsh = LOGN - s0 - LOGE;
@@ -376,10 +380,10 @@ __device__ __forceinline__ void inv_full_pass(const M& md, typename M::T* x, int
 #pragma unroll
   for (int l = LOGE - 1; l >= 0; --l) {
     const int half = G_::E >> (l + 1);
-    const typename M::Tw* twb = itw + (1 << (s0 + l)) + (G << l);
+    const typename M::Tw* twb = itw + (base << (s0 + l)) + (G << l);
 #pragma unroll
     for (int u = 0; u < (1 << l); ++u) {
-      if (s0 + l == 0) {
+      if (s0 + l == 0 && !SUB) {
 #pragma unroll
         for (int e0 = 0; e0 < half; ++e0) {
           const int e = u * 2 * half + e0;
@@ -406,16 +410,19 @@ __device__ __forceinline__ void inv_full_pass(const M& md, typename M::T* x, int
 // thread has consumed its input registers' source by then).
 // FIRST = false: the caller has run the first (register-only) pass itself,
 // e.g. with another twiddle form.
-template <int LOGN, int LOGE, class M, class Hook = NoHook, bool FIRST = true>
+// SUB = true, base = 2^S + g: the transform is sub-block g of a 2^(LOGN+S)-point
+// one (table entries base << stage; its stage 0 is an ordinary butterfly, the
+// N^-1 merge happens in the enclosing transform's last stage).
+template <int LOGN, int LOGE, class M, class Hook = NoHook, bool FIRST = true, bool SUB = false>
 __device__ __forceinline__ void cta_inv(const M& md, typename M::T* x, typename M::T* sm,
                                         const typename M::Tw* __restrict__ itw,
                                         const typename M::Tw& ninv, const typename M::Tw& wn,
                                         const typename M::Tw* __restrict__ itw_last = nullptr,
-                                        const Hook& hook = Hook()) {
+                                        const Hook& hook = Hook(), const int base = 1) {
   typedef Geo<LOGN, LOGE> G_;
   constexpr int LOG_NT = LOGN - LOGE;
   const int tid = threadIdx.x;
-  if (FIRST) inv_last_pass<LOGN, LOGE, M>(md, x, tid, itw_last ? itw_last : itw, ninv, wn);
+  if (FIRST) inv_last_pass<LOGN, LOGE, M, SUB>(md, x, tid, itw_last ? itw_last : itw, ninv, wn, base);
 #pragma unroll
   for (int pass = G_::NFULL - 1; pass >= 0; --pass) {
     // group of this exchange: threads sharing a pass-`pass` region
@@ -434,7 +441,7 @@ __device__ __forceinline__ void cta_inv(const M& md, typename M::T* x, typename 
     group_sync<LOG_NT>(tid, LOGN - (pass + 1) * LOGE);
 #pragma unroll
     for (int e = 0; e < G_::E; ++e) x[e] = sm[xaddr_full<LOGN, LOGE>(pass, tid, e, K, S)];
-    inv_full_pass<LOGN, LOGE, M>(md, x, pass, tid, itw, ninv, wn);
+    inv_full_pass<LOGN, LOGE, M, SUB>(md, x, pass, tid, itw, ninv, wn, base);
   }
 }
 

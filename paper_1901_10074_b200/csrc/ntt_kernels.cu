@@ -5,9 +5,11 @@
 //   * k_ntt32_b / k_ntt64_b: persistent prime-major CTAs (device order);
 //   * k_ntt_fwd / k_ntt_inv: one CTA per polynomial (natural order, small N,
 //     and the 64-bit sizes where that measured faster);
-//   * k_ntt_cl_fwd / k_ntt_cl_inv: polynomials larger than one SM (64-bit
-//     N = 2^15 / 2^16, 30-bit N = 2^16) as one thread-block cluster each,
-//     the CTA-spanning exchange through distributed shared memory;
+//   * k_ntt64_top + k_ntt64_sub: 64-bit N = 2^15 / 2^16 (and the 2^14
+//     forward) as an outer-stage streaming pass plus 2^12-point sub-transforms;
+//   * k_ntt_cl_fwd / k_ntt_cl_inv: 30-bit polynomials larger than one SM
+//     (N = 2^15 / 2^16, the 64-bit key switch's aux basis) as one thread-block
+//     cluster each, the CTA-spanning exchange through distributed shared memory;
 #include <cstdlib>
 
 #include "../../include/hefv.h"
@@ -218,7 +220,13 @@ __global__ void __launch_bounds__(Geo<LOGN, 4>::NT, ntt32_minb<LOGN>())
 #pragma unroll
         for (int e = 0; e < E; ++e) x[e] = barrett62(stage[tid + e * NT], inf.p, inf.mu);
       }
-      if constexpr (LASTSM) {
+      if constexpr (LASTSM && LOGN == 14) {
+        // butterfly sums on the ALU pipe (Mod32A / Mod32MA, modarith.cuh)
+        const Mod32A ma(inf.p);
+        cta_fwd<LOGN, 4, Mod32A, decltype(hook), false>(ma, x, sm, tws, twg, hook);
+        const Mod32MA mm(inf.p, inf.pinv, ma.ones);
+        fwd_last_pass<LOGN, 4, Mod32MA>(mm, x, tid, twl - NTW);
+      } else if constexpr (LASTSM) {
         cta_fwd<LOGN, 4, Mod32, decltype(hook), false>(md, x, sm, tws, twg, hook);
         const Mod32M mm{inf.p, 2 * inf.p, inf.pinv};
         fwd_last_pass<LOGN, 4, Mod32M>(mm, x, tid, twl - NTW);
@@ -347,6 +355,190 @@ static int sm_count() {
   return n;
 }
 
+// ---- 64-bit transforms of 2^13 .. 2^16 points as two HBM passes -------------
+// A 64-bit transform holds its 16 words per thread in 32 registers, so the
+// one-CTA (1024 threads, 64 registers) and cluster forms above 2^12 run
+// register-starved (0.52-0.67 of the butterfly peak) while the 2^12 transform
+// (256 threads, up to 128 registers, several CTAs per SM) reaches 0.82.  The
+// split form runs the S = LOGN - 12 outermost stages as a streaming pass over
+// HBM (k_ntt64_top: 2^S words per thread at stride N / 2^S, coalesced, the
+// 2^S - 1 twiddles uniform) and the remaining 12 stages as 2^S independent
+// 2^12-point sub-transforms per polynomial (k_ntt64_sub: the CTA-resident
+// transform with table entries (2^S + g) << stage for sub-block g).  Same
+// butterfly network and table as the one-kernel forms, hence the same device
+// order and the same canonical outputs.
+template <int S, bool FWD>
+__global__ void __launch_bounds__(256)
+    k_ntt64_top(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, int nprimes,
+                int prime_base, int log_n, const ulonglong2* __restrict__ tw_all,
+                const Prime64Info* __restrict__ info, int bcast) {
+  constexpr int R = 1 << S;
+  const int64_t n = (int64_t)1 << log_n;
+  const int64_t ns = n >> S;                 // element stride between a thread's words
+  const int chunks = (int)(ns >> 8);         // 256-thread blocks per polynomial
+  const int64_t q = blockIdx.x / chunks;     // polynomial (b, j), j fastest
+  const int64_t idx = (int64_t)(blockIdx.x - q * chunks) * 256 + threadIdx.x;
+  const int j = (int)(q % nprimes);
+  const Prime64Info* ip = info + prime_base + j;
+  const uint64_t p = ip->p;
+  const Mod64 md{p, 2 * p};
+  const ulonglong2* tw = tw_all + (size_t)(prime_base + j) * n;
+  const uint64_t* src = in + (bcast ? q / nprimes : q) * n + idx;
+  uint64_t* dst = out + q * n + idx;
+  uint64_t x[R];
+  if constexpr (FWD) {
+#pragma unroll
+    for (int e = 0; e < R; ++e) {
+      const uint64_t v = src[e * ns];
+      x[e] = v >= p ? barrett64(v, p, ip->mu) : v;
+    }
+#pragma unroll
+    for (int l = 0; l < S; ++l) {
+      const int half = R >> (l + 1);
+#pragma unroll
+      for (int u = 0; u < (1 << l); ++u) {
+        const ulonglong2 w = __ldg(tw + (1 << l) + u);
+#pragma unroll
+        for (int e0 = 0; e0 < half; ++e0) md.ct(x[u * 2 * half + e0], x[u * 2 * half + e0 + half], w);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < R; ++e) dst[e * ns] = x[e];  // lazy, < 4p
+  } else {
+#pragma unroll
+    for (int e = 0; e < R; ++e) x[e] = src[e * ns];  // < 2p from k_ntt64_sub
+#pragma unroll
+    for (int l = S - 1; l >= 0; --l) {
+      const int half = R >> (l + 1);
+#pragma unroll
+      for (int u = 0; u < (1 << l); ++u) {
+        if (l == 0) {
+#pragma unroll
+          for (int e0 = 0; e0 < half; ++e0) md.gs_last(x[e0], x[e0 + half], ip->ninv, ip->wn);
+        } else {
+          const ulonglong2 w = __ldg(tw + (1 << l) + u);
+#pragma unroll
+          for (int e0 = 0; e0 < half; ++e0) md.gs(x[u * 2 * half + e0], x[u * 2 * half + e0 + half], w);
+        }
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < R; ++e) dst[e * ns] = md.subp(x[e]);
+  }
+}
+
+// Persistent CTAs over the P = nprimes x 2^S x batch sub-blocks in (prime,
+// sub-block, batch) order, so a CTA keeps one 64 KB twiddle slice hot in L1.
+template <bool FWD>
+__global__ void __launch_bounds__(256, 2)
+    k_ntt64_sub(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, int64_t batch,
+                int nprimes, int prime_base, int log_s, const ulonglong2* __restrict__ tw_all,
+                const Prime64Info* __restrict__ info) {
+  typedef Geo<12, 4> G_;
+  constexpr int E = G_::E;
+  constexpr int NT = G_::NT;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  uint64_t* sm = reinterpret_cast<uint64_t*>(smraw);
+  const int tid = threadIdx.x;
+  const int nsub = 1 << log_s;
+  const int64_t n = (int64_t)G_::N << log_s;
+  const int64_t per_prime = (int64_t)nsub * batch;
+  const int64_t P = per_prime * nprimes;
+  const int64_t qbeg = P * blockIdx.x / gridDim.x;
+  const int64_t qend = P * (blockIdx.x + 1) / gridDim.x;
+  if (qbeg >= qend) return;
+  int j = (int)(qbeg / per_prime);
+  int64_t r = qbeg - (int64_t)j * per_prime;
+  int g = (int)(r / batch);
+  int64_t b = r - (int64_t)g * batch;
+  const int64_t pstride = (int64_t)nprimes * n;
+  for (int64_t q = qbeg; q < qend; ++q) {
+    const Prime64Info* ip = info + prime_base + j;
+    const uint64_t p = ip->p;
+    const Mod64 md{p, 2 * p};
+    const ulonglong2* tw = tw_all + (size_t)(prime_base + j) * n;
+    const int64_t off = b * pstride + (int64_t)j * n + (int64_t)g * G_::N;
+    const int base = nsub + g;
+    // next work item (b fastest, then g, then j)
+    if (++b == batch) {
+      b = 0;
+      if (++g == nsub) {
+        g = 0;
+        ++j;
+      }
+    }
+    if (tid == 0 && q + 1 < qend)
+      bulk_prefetch_l2(in + b * pstride + (int64_t)j * n + (int64_t)g * G_::N, G_::N * 8);
+    uint64_t x[E];
+    if constexpr (FWD) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) x[e] = in[off + tid + e * NT];  // < 4p from k_ntt64_top
+      cta_fwd<12, 4, Mod64>(md, x, sm, tw, nullptr, NoHook(), 0, base);
+#pragma unroll
+      for (int e = 0; e < E; ++e) x[e] = md.canon4(x[e]);
+      store_row_vec<12, 4, uint64_t>(out + off, tid, x);
+    } else {
+      load_row_vec<12, 4, uint64_t>(in + off, tid, x);
+      cta_inv<12, 4, Mod64, NoHook, true, true>(md, x, sm, tw, ip->ninv, ip->wn, nullptr, NoHook(),
+                                                base);
+#pragma unroll
+      for (int e = 0; e < E; ++e) out[off + tid + e * NT] = x[e];  // lazy, < 2p
+    }
+  }
+}
+
+template <int S>
+static int launch_split64_s(bool fwd, const uint64_t* in, uint64_t* out, int64_t batch, int nprimes,
+                            int prime_base, const ulonglong2* tw, const Prime64Info* info,
+                            cudaStream_t st, int bcast) {
+  const int log_n = 12 + S;
+  const int64_t polys = batch * nprimes;
+  const int64_t top_blocks = polys * ((int64_t)1 << (log_n - S - 8));
+  if (top_blocks > 0x7fffffff) return fail("ntt64: batch too large");
+  const size_t smem = (size_t)((spad_size(4096) + 1) & ~1) * 8;
+  auto sub = fwd ? k_ntt64_sub<true> : k_ntt64_sub<false>;
+  HEFV_CUDA(cudaFuncSetAttribute(sub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sub, 256, smem) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  const int64_t P = polys << S;
+  const int64_t slots = (int64_t)sm_count() * per_sm;
+  const unsigned grid = (unsigned)(P < slots ? P : slots);
+  if (fwd) {
+    k_ntt64_top<S, true><<<(unsigned)top_blocks, 256, 0, st>>>(in, out, nprimes, prime_base, log_n,
+                                                                tw, info, bcast);
+    HEFV_LAUNCH_CHECK("k_ntt64_top");
+    sub<<<grid, 256, smem, st>>>(out, out, batch, nprimes, prime_base, S, tw, info);
+    HEFV_LAUNCH_CHECK("k_ntt64_sub");
+  } else {
+    if (bcast) return fail("ntt64: broadcast rows are a forward-only input form");
+    sub<<<grid, 256, smem, st>>>(in, out, batch, nprimes, prime_base, S, tw, info);
+    HEFV_LAUNCH_CHECK("k_ntt64_sub");
+    k_ntt64_top<S, false><<<(unsigned)top_blocks, 256, 0, st>>>(out, out, nprimes, prime_base,
+                                                                 log_n, tw, info, 0);
+    HEFV_LAUNCH_CHECK("k_ntt64_top");
+  }
+  return 0;
+}
+
+static int launch_split64(int log_n, bool fwd, const uint64_t* in, uint64_t* out, int64_t batch,
+                          int nprimes, int prime_base, const ulonglong2* tw,
+                          const Prime64Info* info, cudaStream_t st, int bcast) {
+  switch (log_n) {
+    case 14: return launch_split64_s<2>(fwd, in, out, batch, nprimes, prime_base, tw, info, st, bcast);
+    case 15: return launch_split64_s<3>(fwd, in, out, batch, nprimes, prime_base, tw, info, st, bcast);
+    case 16: return launch_split64_s<4>(fwd, in, out, batch, nprimes, prime_base, tw, info, st, bcast);
+    default: return fail("ntt64 split: N must be 2^14 .. 2^16");
+  }
+}
+
+// Measured (B200, 60-bit, L = 8; fraction of the 64-bit butterfly peak, one-kernel
+// form -> split): 2^16 fwd 0.546 -> 0.719, inv 0.516 -> 0.659; 2^15 0.607 -> 0.692,
+// 0.608 -> 0.643; 2^14 fwd 0.641 -> 0.667 but inv 0.667 -> 0.630; 2^13 loses
+// (0.656 -> 0.636, 0.659 -> 0.601): its single outer stage is not worth an HBM pass.
+static bool ntt64_split(int log_n, bool fwd) { return log_n >= 15 || (log_n == 14 && fwd); }
+
 template <int LOGN>
 static int launch_b32(bool fwd, const uint32_t* in, uint32_t* out, int64_t batch, int nprimes,
                       int prime_base, const uint2* tw, const Prime32Info* info, cudaStream_t st,
@@ -413,6 +605,13 @@ static int launch_one(bool fwd, const typename M::T* in, typename M::T* out, int
                               reinterpret_cast<uint32_t*>(out), batch, nprimes, prime_base,
                               reinterpret_cast<const uint2*>(tw),
                               reinterpret_cast<const Prime32Info*>(info), st, twm);
+  }
+  if constexpr (sizeof(typename M::T) == 8 && LOGN == 14 && LOGE == 4) {
+    if (!natural && ntt64_split(LOGN, fwd))
+      return launch_split64(LOGN, fwd, reinterpret_cast<const uint64_t*>(in),
+                            reinterpret_cast<uint64_t*>(out), batch, nprimes, prime_base,
+                            reinterpret_cast<const ulonglong2*>(tw),
+                            reinterpret_cast<const Prime64Info*>(info), st, bcast);
   }
   if constexpr (sizeof(typename M::T) == 8 && LOGN >= 10 && LOGN <= 14 && LOGE == 4) {
     const int mode = ntt64_mode(LOGN, fwd);
@@ -798,13 +997,6 @@ static int launch_cl(bool fwd, const TIn* in, typename M::T* out, int64_t total_
   return 0;
 }
 
-template <int LOGN>
-static int launch_cl64(bool fwd, const uint64_t* in, uint64_t* out, int64_t total_polys,
-                       int nprimes, int prime_base, const ulonglong2* tw,
-                       const Prime64Info* info, cudaStream_t st, int bcast) {
-  return launch_cl<LOGN, Mod64, uint64_t>(fwd, in, out, total_polys, nprimes, prime_base, tw, info,
-                                          st, bcast);
-}
 
 }  // namespace hefv
 
@@ -815,15 +1007,12 @@ int hefv_ntt64_large(hefv_ctx* c, bool fwd, const uint64_t* in, uint64_t* out, i
   const int64_t total_polys = batch * nprimes;
   if (total_polys <= 0) return 0;
   if (bcast && !(log_n == 15 || log_n == 16))
-    return fail("ntt64: broadcast input rows need the cluster transform");
+    return fail("ntt64: broadcast input rows need N = 2^15 or 2^16");
   if (log_n == 15 || log_n == 16) {
     auto run = [&](const uint64_t* a, uint64_t* b) {
       const ulonglong2* tw = fwd ? c->d_tw64 : c->d_itw64;
-      return log_n == 15
-                 ? launch_cl64<15>(fwd, a, b, total_polys, nprimes, prime_base, tw, c->d_info64, st,
-                                   bcast)
-                 : launch_cl64<16>(fwd, a, b, total_polys, nprimes, prime_base, tw, c->d_info64, st,
-                                   bcast);
+      return launch_split64(log_n, fwd, a, b, batch, nprimes, prime_base, tw, c->d_info64, st,
+                            bcast);
     };
     const int64_t tot = total_polys * n;
     if (!natural) return run(in, out);
@@ -840,8 +1029,8 @@ int hefv_ntt64_large(hefv_ctx* c, bool fwd, const uint64_t* in, uint64_t* out, i
       return 0;
     }
     // natural -> device order into out, then the inverse in place (every CTA
-    // of a cluster loads its input before the first cluster barrier and
-    // stores only after the last one)
+    // of k_ntt64_sub loads its sub-block before it stores, k_ntt64_top is
+    // thread-local)
     k_permute_bitrev64<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(in, out, log_n, tot);
     HEFV_LAUNCH_CHECK("ntt64 permute");
     return run(out, out);
