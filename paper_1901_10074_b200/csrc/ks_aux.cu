@@ -36,6 +36,9 @@
 
 namespace hefv {
 
+#ifndef KSA_ROWSTORE_T
+#define KSA_ROWSTORE_T 1  // phase-1 output through warp_rows_to_chunks (whole 128-byte tile rows)
+#endif
 #ifndef KSA_FWD_CTS_V
 #define KSA_FWD_CTS_V 16
 #endif
@@ -173,7 +176,19 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
     }
 #pragma unroll
     for (int e = 0; e < E; ++e) x[e] = md.canon4(x[e]);
-    store_tiled<LOGN, LOGE>(X + ((size_t)b * 3 + t) * k * (size_t)N, k, i, tid, x);
+    uint32_t* xb = X + ((size_t)b * 3 + t) * k * (size_t)N;
+    if constexpr (LOGE == 4 && KSA_ROWSTORE_T) {
+      // warp-contiguous chunks: 8 lanes write one tile row (128 bytes) whole
+      uint4 c[4];
+      warp_rows_to_chunks(warp_tile_region(sm, tid), tid & 31, x, c);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int p0 = (tid >> 5) * 512 + 4 * (32 * q + (tid & 31));  // first point of the chunk
+        *reinterpret_cast<uint4*>(xb + ((size_t)(p0 >> 5) * k + i) * 32 + (p0 & 31)) = c[q];
+      }
+    } else {
+      store_tiled<LOGN, LOGE>(xb, k, i, tid, x);
+    }
   }
 }
 

@@ -24,6 +24,10 @@
 #pragma once
 #include "modarith.cuh"
 
+#ifndef HEFV_DIAG
+#define HEFV_DIAG 0  // timing diagnostics only (wrong results): 1 no exchange, 2 no group barriers
+#endif
+
 namespace hefv {
 
 // Shared-tile address map: an XOR swizzle of the low 5 bits with bits
@@ -60,6 +64,25 @@ __device__ __forceinline__ int row_index(int tid, int e) {
 // twiddles with 16-byte accesses where possible.
 template <class Tw, int MAXC>
 __device__ __forceinline__ void load_tw_run(const Tw* __restrict__ p, Tw* out, const int count) {
+#if HEFV_DIAG & 4
+  if constexpr (sizeof(Tw) == 8) {
+#pragma unroll
+    for (int i = 0; i < MAXC; ++i) {
+      uint2 v = make_uint2(123456789u + 977u * i, 493903u + 13u * i);
+      asm volatile("" : "+r"(v.x), "+r"(v.y));
+      out[i] = *reinterpret_cast<Tw*>(&v);
+    }
+    return;
+  } else if constexpr (sizeof(Tw) == 4) {
+#pragma unroll
+    for (int i = 0; i < MAXC; ++i) {
+      uint32_t v = 123456789u + 977u * i;
+      asm volatile("" : "+r"(v));
+      out[i] = *reinterpret_cast<Tw*>(&v);
+    }
+    return;
+  }
+#endif
   if (sizeof(Tw) == 4 && count % 4 == 0) {  // single-word (Montgomery) twiddles
     const uint4* q = reinterpret_cast<const uint4*>(p);
 #pragma unroll
@@ -286,12 +309,17 @@ __device__ __forceinline__ void cta_fwd(const M& md, typename M::T* x, typename 
       __syncthreads();
       hook();
     } else {
+#if !(HEFV_DIAG & 2)
       group_sync<LOG_NT>(tid, LOGN - (pass + 1) * LOGE);
+#endif
     }
+#if !(HEFV_DIAG & 1)
     const int K = xpad_k(LOGN, LOGE, pass), S = xpad_s(LOGN, LOGE, pass);
 #pragma unroll
     for (int e = 0; e < G_::E; ++e) sm[xaddr_full<LOGN, LOGE>(pass, tid, e, K, S)] = x[e];
+#if !(HEFV_DIAG & 2)
     group_sync<LOG_NT>(tid, LOGN - (pass + 1) * LOGE);
+#endif
     if (pass + 1 < G_::NFULL) {
 #pragma unroll
       for (int e = 0; e < G_::E; ++e) x[e] = sm[xaddr_full<LOGN, LOGE>(pass + 1, tid, e, K, S)];
@@ -299,6 +327,7 @@ __device__ __forceinline__ void cta_fwd(const M& md, typename M::T* x, typename 
 #pragma unroll
       for (int e = 0; e < G_::E; ++e) x[e] = sm[xaddr_row<LOGN, LOGE>(tid, e, K, S)];
     }
+#endif
   }
   // last pass: stages with table entries below 2^split_log from `tw`, the rest from tw_last
   // (LAST = false: the caller runs it, e.g. with another twiddle form)
@@ -428,6 +457,14 @@ __device__ __forceinline__ void cta_inv(const M& md, typename M::T* x, typename 
     // group of this exchange: threads sharing a pass-`pass` region
     // this exchange is the inverse of forward exchange `pass`: same padding
     const int K = xpad_k(LOGN, LOGE, pass), S = xpad_s(LOGN, LOGE, pass);
+#if HEFV_DIAG & 1
+    if (pass == G_::NFULL - 1) {
+      __syncthreads();
+      hook();
+    }
+    (void)K;
+    (void)S;
+#else
     if (pass == G_::NFULL - 1) {
       __syncthreads();  // the tile may still be in use by a previous transform
       hook();
@@ -441,6 +478,7 @@ __device__ __forceinline__ void cta_inv(const M& md, typename M::T* x, typename 
     group_sync<LOG_NT>(tid, LOGN - (pass + 1) * LOGE);
 #pragma unroll
     for (int e = 0; e < G_::E; ++e) x[e] = sm[xaddr_full<LOGN, LOGE>(pass, tid, e, K, S)];
+#endif
     inv_full_pass<LOGN, LOGE, M, SUB>(md, x, pass, tid, itw, ninv, wn, base);
   }
 }
@@ -507,6 +545,84 @@ __device__ __forceinline__ void load_row_vec(const T* __restrict__ base, int tid
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = p[e];
   }
+}
+
+// Row-layout registers (16 consecutive words per thread) -> warp-contiguous
+// 16-byte chunks, through the warp's own 512-word region of the exchange tile:
+// chunk c[i] of lane L is words [4 (32 i + L), +4) of the warp's 512 words, so a
+// 128-bit global store of c[i] by the whole warp covers 512 contiguous bytes
+// (storing the row layout directly puts each lane's 16 bytes in a different
+// 64-byte run: 16 partial lines per instruction; measured 14 % of the 2^14
+// forward).  Thread T's quad q sits at quad position q ^ ((T >> 1) & 3): both
+// the 128-bit writes and the 128-bit reads are bank-conflict free without
+// register selects.  `wbuf` must be private to the warp at this point (true
+// after the forward's last exchange, which is warp-local) and 16-byte aligned.
+__device__ __forceinline__ void warp_rows_to_chunks(uint32_t* wbuf, int lane, const uint32_t* x,
+                                                    uint4* c) {
+  const int r = (lane >> 1) & 3;
+  uint4* mine = reinterpret_cast<uint4*>(wbuf + lane * 16);
+  __syncwarp();  // every lane has read its exchange data out of the region
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    mine[q ^ r] = make_uint4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int ch = i * 32 + lane;
+    const int T = ch >> 2;
+    c[i] = reinterpret_cast<const uint4*>(wbuf + T * 16)[(ch & 3) ^ ((T >> 1) & 3)];
+  }
+}
+// 64-bit words: 16 consecutive words per thread are 8 quads of 16 bytes; thread
+// T's quad q sits at position q ^ (T & 7).  rows -> chunks (forward output):
+// chunk c[i] of lane L is bytes [16 (32 i + L), +16) of the warp's 4 KB.
+__device__ __forceinline__ void warp_rows_to_chunks64(uint64_t* wbuf, int lane, const uint64_t* x,
+                                                      uint4* c) {
+  const int r = lane & 7;
+  uint4* mine = reinterpret_cast<uint4*>(wbuf + lane * 16);
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    uint4 v;
+    v.x = (uint32_t)x[2 * q];
+    v.y = (uint32_t)(x[2 * q] >> 32);
+    v.z = (uint32_t)x[2 * q + 1];
+    v.w = (uint32_t)(x[2 * q + 1] >> 32);
+    mine[q ^ r] = v;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int ch = i * 32 + lane;
+    const int T = ch >> 3;
+    c[i] = reinterpret_cast<const uint4*>(wbuf + T * 16)[(ch & 7) ^ (T & 7)];
+  }
+}
+// chunks -> rows (inverse input): the caller loaded chunk c[i] = bytes
+// [16 (32 i + L), +16) of the warp's 4 KB with coalesced 128-bit loads; `wbuf`
+// must not be in use by any other warp (CTA barrier before the call).
+__device__ __forceinline__ void warp_chunks_to_rows64(uint64_t* wbuf, int lane, const uint4* c,
+                                                      uint64_t* x) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int ch = i * 32 + lane;
+    const int T = ch >> 3;
+    reinterpret_cast<uint4*>(wbuf + T * 16)[(ch & 7) ^ (T & 7)] = c[i];
+  }
+  __syncwarp();
+  const int r = lane & 7;
+  const uint4* mine = reinterpret_cast<const uint4*>(wbuf + lane * 16);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const uint4 v = mine[q ^ r];
+    x[2 * q] = ((uint64_t)v.y << 32) | v.x;
+    x[2 * q + 1] = ((uint64_t)v.w << 32) | v.z;
+  }
+}
+// the warp's region of the tile after the last (1/16-padded) exchange
+template <class T>
+__device__ __forceinline__ T* warp_tile_region(T* sm, int tid) {
+  return sm + (tid >> 5) * 544;
 }
 
 // Row-layout read of 16 consecutive 32-bit words per thread from SHARED

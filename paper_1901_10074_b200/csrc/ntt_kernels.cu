@@ -20,6 +20,10 @@
 
 namespace hefv {
 
+#ifndef NTT64_ROWIO
+#define NTT64_ROWIO 1  // 64-bit row-layout global I/O through warp-contiguous chunks
+#endif
+
 // transform input -> lazy range: 64-bit primes any u64; 30-bit primes from
 // u32 or from u64 < 2^62 (the 64-bit key switch's digits)
 __device__ __forceinline__ uint64_t cl_in(uint64_t v, const Prime64Info& i) {
@@ -57,7 +61,15 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT)
 #pragma unroll
   for (int e = 0; e < G_::E; ++e) x[e] = md.canon4(x[e]);
   if (!natural) {
-    store_row_vec<LOGN, LOGE, T>(dst, tid, x);
+    if constexpr (sizeof(T) == 8 && LOGE == 4 && G_::NT >= 32 && NTT64_ROWIO) {
+      uint4 c[8];  // warp-contiguous 128-bit stores (see k_ntt64_sub)
+      warp_rows_to_chunks64(warp_tile_region(sm, tid), tid & 31, x, c);
+      uint4* d4 = reinterpret_cast<uint4*>(dst + (tid >> 5) * 512) + (tid & 31);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) d4[32 * i] = c[i];
+    } else {
+      store_row_vec<LOGN, LOGE, T>(dst, tid, x);
+    }
   } else {
     // dev index i holds natural index bitrev(i): stage through smem
     __syncthreads();
@@ -120,6 +132,9 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT)
 // 0.63 of the butterfly peak, forward unchanged; measured on a B200)
 #ifndef NTT32_LASTSM_MASK
 #define NTT32_LASTSM_MASK ((1 << 14) | (1 << 12))
+#endif
+#ifndef ROWSTORE_T
+#define ROWSTORE_T 1  // forward output through warp_rows_to_chunks (coalesced 128-bit stores)
 #endif
 #ifndef NTT32_MINB_SMALL
 #define NTT32_MINB_SMALL 0  // 0: 1024 / NT resident CTAs per SM for N <= 2^12
@@ -196,17 +211,26 @@ __global__ void __launch_bounds__(Geo<LOGN, 4>::NT, ntt32_minb<LOGN>())
       __syncthreads();
     }
     const Mod32 md{inf.p, 2 * inf.p};
+#if !(HEFV_DIAG & 16)
     mbar_wait(mbar, phase);
     phase ^= 1u;
+#endif
     uint32_t x[E];
+#if HEFV_DIAG & 16
+    const uint32_t* nxt = nullptr;
+#else
     const uint32_t* nxt = q + 1 < qend ? in + poly(q + 1) : nullptr;
+#endif
     auto hook = [&]() {
       if (tid == 0 && nxt) bulk_g2s(stage, nxt, N * 4, mbar);
     };
     if constexpr (FWD) {
       // input -> [0, 4p): the prime's class is uniform, so branch once around
       // the 16 loads (a per-element branch costs ~8 issue slots per word)
-      if (inf.p >= (1u << 30)) {
+      if (HEFV_DIAG & 16) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) x[e] = (uint32_t)(tid * 977 + e * 131 + (int)q);
+      } else if (inf.p >= (1u << 30)) {
 #pragma unroll
         for (int e = 0; e < E; ++e) x[e] = stage[tid + e * NT];
       } else if (inf.p > (1u << 29)) {
@@ -233,11 +257,31 @@ __global__ void __launch_bounds__(Geo<LOGN, 4>::NT, ntt32_minb<LOGN>())
       } else {
         cta_fwd<LOGN, 4, Mod32>(md, x, sm, tws, twg, hook, LOGN - G_::RLAST);
       }
+#if HEFV_DIAG & 8
+      uint32_t acc = 0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc ^= x[e];
+      if (acc == 0x12345u) out[poly(q) + tid] = acc;
+#else
 #pragma unroll
       for (int e = 0; e < E; ++e) x[e] = md.canon4(x[e]);
-      store_row_vec<LOGN, 4, uint32_t>(out + poly(q), tid, x);
+      if constexpr (NT >= 32 && ROWSTORE_T) {
+        uint4 c[4];
+        warp_rows_to_chunks(warp_tile_region(sm, tid), tid & 31, x, c);
+        uint4* dst = reinterpret_cast<uint4*>(out + poly(q) + (tid >> 5) * 512) + (tid & 31);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dst[32 * i] = c[i];
+      } else {
+        store_row_vec<LOGN, 4, uint32_t>(out + poly(q), tid, x);
+      }
+#endif
     } else {
+#if HEFV_DIAG & 16
+#pragma unroll
+      for (int e = 0; e < E; ++e) x[e] = (uint32_t)(tid * 977 + e * 131 + (int)q) & 0xfffffffu;
+#else
       load_row16_smem(stage, tid, x);
+#endif
       if constexpr (LASTSM) {
         const Mod32M mm{inf.p, 2 * inf.p, inf.pinv};
         inv_last_pass<LOGN, 4, Mod32M>(mm, x, tid, twl - NTW, 0u, 0u);  // N^-1 is in pass 0
@@ -246,8 +290,15 @@ __global__ void __launch_bounds__(Geo<LOGN, 4>::NT, ntt32_minb<LOGN>())
         cta_inv<LOGN, 4, Mod32>(md, x, sm, tws, inf.ninv, inf.wn, twg, hook);
       }
       uint32_t* dst = out + poly(q);
+#if HEFV_DIAG & 8
+      uint32_t acc = 0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc ^= x[e];
+      if (acc == 0x12345u) dst[tid] = acc;
+#else
 #pragma unroll
       for (int e = 0; e < E; ++e) dst[tid + e * NT] = md.subp(x[e]);
+#endif
     }
   }
 }
@@ -334,9 +385,27 @@ __global__ void __launch_bounds__(Geo<LOGN, 4>::NT, LOGN >= 13 ? 1024 / Geo<LOGN
       cta_fwd<LOGN, 4, Mod64>(md, x, sm, twf, twg, NoHook(), LOGN - G_::RLAST);
 #pragma unroll
       for (int e = 0; e < E; ++e) x[e] = md.canon4(x[e]);
-      store_row_vec<LOGN, 4, uint64_t>(dst, tid, x);
+      if constexpr (NTT64_ROWIO) {
+        uint4 c[8];  // warp-contiguous 128-bit stores (see k_ntt64_sub)
+        warp_rows_to_chunks64(warp_tile_region(sm, tid), tid & 31, x, c);
+        uint4* d4 = reinterpret_cast<uint4*>(dst + (tid >> 5) * 512) + (tid & 31);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) d4[32 * i] = c[i];
+      } else {
+        store_row_vec<LOGN, 4, uint64_t>(dst, tid, x);
+      }
     } else {
-      load_row_vec<LOGN, 4, uint64_t>(src, tid, x);
+      // (2^13: the chunk registers spill at 64 registers per thread, 0.659 -> 0.626)
+      if constexpr (NTT64_ROWIO && LOGN == 14) {
+        uint4 c[8];
+        const uint4* s4 = reinterpret_cast<const uint4*>(src + (tid >> 5) * 512) + (tid & 31);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) c[i] = __ldg(s4 + 32 * i);
+        __syncthreads();  // the previous transform's last exchange has been read
+        warp_chunks_to_rows64(warp_tile_region(sm, tid), tid & 31, c, x);
+      } else {
+        load_row_vec<LOGN, 4, uint64_t>(src, tid, x);
+      }
       cta_inv<LOGN, 4, Mod64>(md, x, sm, twf, ip->ninv, ip->wn, twg);
 #pragma unroll
       for (int e = 0; e < E; ++e) dst[tid + e * NT] = md.subp(x[e]);
@@ -476,9 +545,20 @@ __global__ void __launch_bounds__(256, 2)
       cta_fwd<12, 4, Mod64>(md, x, sm, tw, nullptr, NoHook(), 0, base);
 #pragma unroll
       for (int e = 0; e < E; ++e) x[e] = md.canon4(x[e]);
-      store_row_vec<12, 4, uint64_t>(out + off, tid, x);
+      // warp-contiguous 128-bit stores (a row-layout store puts each lane's 16
+      // bytes in a different 128-byte line)
+      uint4 c[8];
+      warp_rows_to_chunks64(warp_tile_region(sm, tid), tid & 31, x, c);
+      uint4* dst = reinterpret_cast<uint4*>(out + off + (tid >> 5) * 512) + (tid & 31);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dst[32 * i] = c[i];
     } else {
-      load_row_vec<12, 4, uint64_t>(in + off, tid, x);
+      uint4 c[8];
+      const uint4* src = reinterpret_cast<const uint4*>(in + off + (tid >> 5) * 512) + (tid & 31);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) c[i] = __ldg(src + 32 * i);
+      __syncthreads();  // the previous transform's last exchange has been read
+      warp_chunks_to_rows64(warp_tile_region(sm, tid), tid & 31, c, x);
       cta_inv<12, 4, Mod64, NoHook, true, true>(md, x, sm, tw, ip->ninv, ip->wn, nullptr, NoHook(),
                                                 base);
 #pragma unroll

@@ -13,6 +13,8 @@
 //   kind 7: DFMA (fp64 fused multiply-add)
 //   kind 8: the kind-4 butterfly with its quotient on the FP64 pipe
 //   kind 9: kinds 4 and 8 interleaved (half the chains each)
+//   kind 10: VIADDMNMX (min(a, a - b), the butterflies' conditional subtract)
+//   kind 11: LOP3 + add pair, kind 12: LOP3 + VIADDMNMX pair (ALU-pipe rates)
 // Each thread runs 8 independent chains so the pipes, not latency, bound it.
 #include "../../include/hefv.h"
 #include "internal.h"
@@ -72,6 +74,13 @@ __global__ void __launch_bounds__(256) k_probe(uint32_t* out, int iters, uint32_
           a[i] = (uint32_t)t ^ (uint32_t)(t >> 32);
         } else if (KIND == 3) {
           a[i] = a[i] + b[i] + 0x777u;
+        } else if (KIND == 10) {
+          a[i] = min(a[i], a[i] - b[i]);  // VIADDMNMX (the butterflies' conditional subtract)
+        } else if (KIND == 11) {
+          a[i] = (a[i] ^ b[i]) + b[i];  // LOP3 + add (counted as 1 op)
+        } else if (KIND == 12) {
+          const uint32_t v = a[i] ^ b[i];  // LOP3 + VIADDMNMX (counted as 1 op)
+          a[i] = min(v, v - p2);
         } else if (KIND == 8 || (KIND == 9 && (i & 1))) {
           // the same butterfly with the Shoup quotient taken on the FP64
           // pipe: q = rint(y * w / p) from y as an exact double (magic-
@@ -383,6 +392,15 @@ extern "C" int hefv_probe_int(int32_t kind, int32_t blocks, int32_t iters, uint3
       break;
     case 9:
       k_probe<9><<<blocks, 256, 0, st>>>(out, iters, 7u);
+      break;
+    case 10:
+      k_probe<10><<<blocks, 256, 0, st>>>(out, iters, 7u);
+      break;
+    case 11:
+      k_probe<11><<<blocks, 256, 0, st>>>(out, iters, 7u);
+      break;
+    case 12:
+      k_probe<12><<<blocks, 256, 0, st>>>(out, iters, 7u);
       break;
     default:
       return fail("hefv_probe_int: unknown kind");
