@@ -36,6 +36,11 @@
 
 namespace hefv {
 
+#ifndef KSA_DIAG
+#define KSA_DIAG 0  // timing diagnostics only (wrong results): 1 inv no CRT, 2 inv no output,
+                    // 4 inv no input, 8 mac no store, 16 fwd no output, 32 fwd no input,
+                    // 64 mac digits from registers (no ring waits / shared loads)
+#endif
 #ifndef KSA_ROWSTORE_T
 #define KSA_ROWSTORE_T 1  // phase-1 output through warp_rows_to_chunks (whole 128-byte tile rows)
 #endif
@@ -148,7 +153,10 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
     phase ^= 1u;
     uint32_t x[E];
     // c_i < p_i < 2^30 <= 4 a_t: a valid lazy input
-    if (ginv) {
+    if (KSA_DIAG & 32) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) x[e] = (uint32_t)(tid * 977 + e * 131 + (int)b) & 0xfffffffu;
+    } else if (ginv) {
       // fused Galois automorphism x -> x^g (fv.py:157-173): coefficient m of
       // sigma(c) is c[m g^-1 mod 2N], negated mod p_i when that index >= N
 #pragma unroll
@@ -177,6 +185,12 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
 #pragma unroll
     for (int e = 0; e < E; ++e) x[e] = md.canon4(x[e]);
     uint32_t* xb = X + ((size_t)b * 3 + t) * k * (size_t)N;
+    if (KSA_DIAG & 16) {
+      uint32_t a2 = 0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) a2 ^= x[e];
+      if (a2 == 0x12345u) xb[tid] = a2;
+    } else
     if constexpr (LOGE == 4 && KSA_ROWSTORE_T) {
       // warp-contiguous chunks: 8 lanes write one tile row (128 bytes) whole
       uint4 c[4];
@@ -395,15 +409,20 @@ __global__ void __launch_bounds__(32 * (JW + 1 + ksa_pw(JW)), 1)
   for (int r = 0; r < nb; r += 2) {
     const int st0 = r % S, st1 = (r + 1) % S;
     const bool two = r + 1 < nb;
-    mbw(xready0 + 8 * st0, (uint32_t)((r / S) & 1));
-    if (two) mbw(xready0 + 8 * st1, (uint32_t)(((r + 1) / S) & 1));
+    if (!(KSA_DIAG & 64)) {
+      mbw(xready0 + 8 * st0, (uint32_t)((r / S) & 1));
+      if (two) mbw(xready0 + 8 * st1, (uint32_t)(((r + 1) / S) & 1));
+    }
     const uint2* xs0 = &xx[st0][0][lane];
     const uint2* xs1 = &xx[st1][0][lane];
     uint64_t b0 = 0, m0 = 0, b1 = 0, m1 = 0;
+    uint32_t dg = (uint32_t)r + lane;
+    if (KSA_DIAG & 64) asm volatile("" : "+r"(dg));
 #pragma unroll
     for (int u = 0; u < H; ++u) {
-      const uint2 xv0 = xs0[32 * u];
-      const uint2 xv1 = two ? xs1[32 * u] : make_uint2(0u, 0u);
+      const uint2 xv0 = (KSA_DIAG & 64) ? make_uint2(dg + u, dg ^ (u * 77)) : xs0[32 * u];
+      const uint2 xv1 = (KSA_DIAG & 64) ? make_uint2(dg - u, dg ^ (u * 55))
+                                        : (two ? xs1[32 * u] : make_uint2(0u, 0u));
       uint64_t kbu, kmu;
       if constexpr (ALLS) {
         kbu = kmw[(2 * u) * JW * 32];
@@ -428,6 +447,11 @@ __global__ void __launch_bounds__(32 * (JW + 1 + ksa_pw(JW)), 1)
       mba(xempty0 + 8 * st0);
       if (two) mba(xempty0 + 8 * st1);
     }
+    if (KSA_DIAG & 8) {
+      const uint32_t a2 = red(b0 - xp0 - kpb) ^ red(m0 - xp0 - kpm) ^ red(b1 - xp1 - kpb) ^
+                          red(m1 - xp1 - kpm);
+      if (a2 == 0x12345u) yb[0] = a2;
+    } else
     if (active) {
       yb[0] = red(b0 - xp0 - kpb);
       yb[ymask] = red(m0 - xp0 - kpm);
@@ -539,7 +563,10 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
       const Mod32 ma{pa.p, 2 * pa.p};
       mbar_wait(mbar, phase);
       phase ^= 1u;
-      if constexpr (LOGE == 4)
+      if (KSA_DIAG & 4) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) x[e] = (uint32_t)(tid * 977 + e * 131 + t) & 0xfffffffu;
+      } else if constexpr (LOGE == 4)
         load_row16_smem(stage, tid, x);
       else
         load_row_vec<LOGN, LOGE>(stage, tid, x);
@@ -556,6 +583,10 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
                                  nullptr, hook);
       const uint2 c = t == 0 ? cc.c[0] : (t == 1 ? cc.c[1] : cc.c[2]);
       const uint32_t qs = t == 0 ? ct.qs[0] : (t == 1 ? ct.qs[1] : ct.qs[2]);
+      if (KSA_DIAG & 1) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[e] = t ? acc[e] ^ x[e] : x[e];
+      } else
 #pragma unroll
       for (int q = 0; q < E / 8; ++q) {
         uint4 vv = t ? vsum[q * NT + tid] : make_uint4(0u, 0u, 0u, 0u);
@@ -572,6 +603,13 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
         }
         vsum[q * NT + tid] = vv;
       }
+    }
+    if (KSA_DIAG & 2) {
+      uint32_t a2 = 0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) a2 ^= acc[e];
+      if (a2 == 0x12345u) out0[tid] = a2;
+      continue;
     }
     const int64_t s = slot ? (int64_t)slot[b] : b;
     uint32_t* o = (part ? out1 : out0) + s * out_stride + (size_t)j * N;

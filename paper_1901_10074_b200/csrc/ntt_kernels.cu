@@ -496,10 +496,13 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+#ifndef NTT64_SUB_MINB
+#define NTT64_SUB_MINB 2  // resident CTAs per SM the sub-transform is compiled for
+#endif
 // Persistent CTAs over the P = nprimes x 2^S x batch sub-blocks in (prime,
 // sub-block, batch) order, so a CTA keeps one 64 KB twiddle slice hot in L1.
 template <bool FWD>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, NTT64_SUB_MINB)
     k_ntt64_sub(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, int64_t batch,
                 int nprimes, int prime_base, int log_s, const ulonglong2* __restrict__ tw_all,
                 const Prime64Info* __restrict__ info) {
