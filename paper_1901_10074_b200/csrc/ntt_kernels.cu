@@ -133,6 +133,12 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT)
 #ifndef NTT32_LASTSM_MASK
 #define NTT32_LASTSM_MASK ((1 << 14) | (1 << 12))
 #endif
+#ifndef NTT32_ALLSM_MASK
+// N whose whole Shoup table (8 N bytes) is staged in shared memory: at 2^12 a third
+// of the butterflies are in the last pass, and Shoup pairs for it (3 CTAs of 65 KB
+// per SM) beat the Montgomery words (4 CTAs of 50 KB): forward 0.588 -> 0.604
+#define NTT32_ALLSM_MASK (1 << 12)
+#endif
 #ifndef ROWSTORE_T
 #define ROWSTORE_T 1  // forward output through warp_rows_to_chunks (coalesced 128-bit stores)
 #endif
@@ -141,6 +147,7 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT)
 #endif
 template <int LOGN>
 constexpr int ntt32_minb() {
+  if (((NTT32_ALLSM_MASK >> LOGN) & 1) && LOGN == 12) return 3;  // 65 KB per CTA
   return (Geo<LOGN, 4>::NT <= 256 && NTT32_MINB_SMALL) ? NTT32_MINB_SMALL
                                                        : 1024 / Geo<LOGN, 4>::NT;
 }
@@ -149,8 +156,9 @@ template <int LOGN, bool FWD>
 struct Ntt32B {
   typedef Geo<LOGN, 4> G_;
   // fwd: last pass; inv: its first pass
-  static constexpr bool LASTSM = ((NTT32_LASTSM_MASK >> LOGN) & 1) != 0;
-  static constexpr int NTW = 1 << (LOGN - G_::RLAST);
+  static constexpr bool ALLSM = ((NTT32_ALLSM_MASK >> LOGN) & 1) != 0;
+  static constexpr bool LASTSM = !ALLSM && ((NTT32_LASTSM_MASK >> LOGN) & 1) != 0;
+  static constexpr int NTW = ALLSM ? G_::N : 1 << (LOGN - G_::RLAST);
   static constexpr size_t smem = (size_t)NTW * sizeof(uint2) +
                                  (size_t)((spad_size(G_::N) + 3) & ~3) * 4 + (size_t)G_::N * 4 +
                                  16 + (LASTSM ? (size_t)(G_::N - NTW) * 4 : 0);
@@ -165,8 +173,9 @@ __global__ void __launch_bounds__(Geo<LOGN, 4>::NT, ntt32_minb<LOGN>())
   constexpr int E = G_::E;
   constexpr int NT = G_::NT;
   constexpr int N = G_::N;
-  constexpr int NTW = 1 << (LOGN - G_::RLAST);
+  constexpr int NTW = Ntt32B<LOGN, FWD>::NTW;
   constexpr bool LASTSM = Ntt32B<LOGN, FWD>::LASTSM;
+  constexpr bool ALLSM = Ntt32B<LOGN, FWD>::ALLSM;
   extern __shared__ __align__(16) unsigned char smraw[];
   uint2* tws = reinterpret_cast<uint2*>(smraw);
   uint32_t* sm = reinterpret_cast<uint32_t*>(tws + NTW);
@@ -254,6 +263,8 @@ __global__ void __launch_bounds__(Geo<LOGN, 4>::NT, ntt32_minb<LOGN>())
         cta_fwd<LOGN, 4, Mod32, decltype(hook), false>(md, x, sm, tws, twg, hook);
         const Mod32M mm{inf.p, 2 * inf.p, inf.pinv};
         fwd_last_pass<LOGN, 4, Mod32M>(mm, x, tid, twl - NTW);
+      } else if constexpr (ALLSM) {
+        cta_fwd<LOGN, 4, Mod32>(md, x, sm, tws, nullptr, hook);
       } else {
         cta_fwd<LOGN, 4, Mod32>(md, x, sm, tws, twg, hook, LOGN - G_::RLAST);
       }
@@ -286,6 +297,8 @@ __global__ void __launch_bounds__(Geo<LOGN, 4>::NT, ntt32_minb<LOGN>())
         const Mod32M mm{inf.p, 2 * inf.p, inf.pinv};
         inv_last_pass<LOGN, 4, Mod32M>(mm, x, tid, twl - NTW, 0u, 0u);  // N^-1 is in pass 0
         cta_inv<LOGN, 4, Mod32, decltype(hook), false>(md, x, sm, tws, inf.ninv, inf.wn, twg, hook);
+      } else if constexpr (ALLSM) {
+        cta_inv<LOGN, 4, Mod32>(md, x, sm, tws, inf.ninv, inf.wn, nullptr, hook);
       } else {
         cta_inv<LOGN, 4, Mod32>(md, x, sm, tws, inf.ninv, inf.wn, twg, hook);
       }
