@@ -63,6 +63,7 @@ struct hefv_ctx {
   // aux-basis key switch (hefv_ks_aux_setup): three ~28-bit NTT primes at
   // primes32[ksa_base, ksa_base + 3)
   bool ksa_ready = false;
+  bool ksa_shiftq = false;  // aux primes within 2^28 (1 + 1/16): CRT quotient terms by a shift
   int ksa_base = -1;
   hefv::KsaJ* d_ksa_j = nullptr;
   hefv::KsaT ksa_t{};

@@ -518,7 +518,12 @@ __global__ void __launch_bounds__(32 * (JW + 1 + ksa_pw(JW)), 1)
 // barrier).  The quotient estimate sum_t y_t / a_t is accumulated as
 // 2^14-scaled fixed point (16 bits per coefficient, error < 3 * 2^-14, far
 // inside the 3/8 rounding margin).
-template <int LOGN, int LOGE>
+// SHIFTQ: every aux prime lies in (2^28, 2^28 (1 + 1/16)), so floor(y 2^14 / a_t)
+// is taken as y >> 14 (an ALU shift instead of an IMAD.HI): that over-estimates a
+// term by < y_t / a_t / 16, the sum of three by < 3/16, and with the truncations
+// (3 * 2^-14) the estimate stays within (-0.001, 0.19) of the true sum, which
+// itself lies within 1/8 of the integer v -- rint still returns v.
+template <int LOGN, int LOGE, bool SHIFTQ>
 __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
     k_ksa_inv(const uint32_t* __restrict__ Y, uint32_t* out0, uint32_t* out1, int64_t out_stride,
               const int32_t* __restrict__ slot, const uint32_t* __restrict__ adA0,
@@ -596,7 +601,7 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT, 1)
           const int e = 8 * q + r;
           const uint32_t y = ma.subp(x[e]);
           // y * 2^14 / a_t, rounded down (< 2^14): 16-bit lanes never carry
-          const uint32_t f = __umulhi(y, qs);
+          const uint32_t f = SHIFTQ ? (y >> 14) : __umulhi(y, qs);
           vw[r >> 1] += (r & 1) ? (f << 16) : f;
           const uint32_t m = Mod32::mul_shoup(y, c.x, c.y, pj.p);  // [0, 2 p_j)
           acc[e] = t ? mj.sub2p(acc[e] + m) : m;
@@ -722,7 +727,7 @@ static int run_ksa_e(hefv_ctx* c, const uint32_t* kaux, const uint32_t* dig, int
   const int64_t n = c->n;
   const int ab = c->ksa_base;
   auto kf = k_ksa_fwd<LOGN, LF>;
-  auto ki = k_ksa_inv<LOGN, LI>;
+  auto ki = c->ksa_shiftq ? k_ksa_inv<LOGN, LI, true> : k_ksa_inv<LOGN, LI, false>;
   const size_t tile = (size_t)((spad_size(GF::N) + 3) & ~3) * 4;
   const size_t smf = KsaFwdSmem<LOGN, LF>::bytes;
   const size_t smi = tile + (size_t)GI::N * 2 + (size_t)GI::N * 4 + 16;
@@ -908,6 +913,9 @@ int hefv_ks_aux_setup(hefv_ctx* c, int32_t aux_base) {
   HEFV_CUDA(cudaMalloc(&c->d_ksa_j, cj.size() * sizeof(KsaJ)));
   HEFV_CUDA(cudaMemcpy(c->d_ksa_j, cj.data(), cj.size() * sizeof(KsaJ), cudaMemcpyHostToDevice));
   c->ksa_t = ct;
+  c->ksa_shiftq = true;
+  for (int t = 0; t < 3; ++t)
+    if (a[t] >= (1u << 28) + (1u << 24)) c->ksa_shiftq = false;
   c->ksa_base = aux_base;
   c->ksa_ready = true;
   return 0;

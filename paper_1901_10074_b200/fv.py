@@ -34,6 +34,11 @@ from .ring import (
     slot_to_eval,
 )
 
+# The aux-basis key switch's three NTT primes are the largest below
+# 2^28 (1 + 1/16): above 2^28 (valid lazy inputs, Montgomery bound) and close
+# enough to it that ks_aux.cu takes the CRT quotient terms by a shift.
+KS_AUX_BELOW = (1 << 28) + (1 << 24)
+
 SIGMA = 3.2
 ERR_BOUND = 19  # 6-sigma truncation (fv.py:25-26)
 
@@ -115,7 +120,7 @@ class FvContext:
 
         self.ks_aux = (8 < self.k <= 24 and 10 <= self.log_n <= 14
                        and os.environ.get("HEFV_KS_AUX", "1") != "0")
-        self.ks_aux_primes = (find_ntt_primes(3, 29, 2 * n, below=int(2 ** 28.25))
+        self.ks_aux_primes = (find_ntt_primes(3, 29, 2 * n, below=KS_AUX_BELOW)
                               if self.ks_aux else [])
         primes32 = self.q_primes + self.aux_primes + self.ks_aux_primes
         psi32 = [root_of_unity(p, n) for p in primes32]
