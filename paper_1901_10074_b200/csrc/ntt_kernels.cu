@@ -7,9 +7,10 @@
 //     and the 64-bit sizes where that measured faster);
 //   * k_ntt64_top + k_ntt64_sub: 64-bit N = 2^15 / 2^16 (and the 2^14
 //     forward) as an outer-stage streaming pass plus 2^12-point sub-transforms;
-//   * k_ntt_cl_fwd / k_ntt_cl_inv: 30-bit polynomials larger than one SM
-//     (N = 2^15 / 2^16, the 64-bit key switch's aux basis) as one thread-block
-//     cluster each, the CTA-spanning exchange through distributed shared memory;
+//   * k_ntt32_top + k_ntt32_b<14, ., SUB>: 30-bit N = 2^16 the same way;
+//   * k_ntt_cl_fwd: 30-bit N = 2^15 rows of the 64-bit key switch's aux basis as
+//     one 2-CTA thread-block cluster each, the CTA-spanning exchange through
+//     distributed shared memory;
 #include <cstdlib>
 
 #include "../../include/hefv.h"
@@ -164,11 +165,19 @@ struct Ntt32B {
                                  16 + (LASTSM ? (size_t)(G_::N - NTW) * 4 : 0);
 };
 
-template <int LOGN, bool FWD>
+// SUB (N = 2^14 only): the polynomials are the 2^log_s sub-blocks of 2^(14 + log_s)-
+// point ones (k_ntt32_top ran, or will run, the log_s outer stages): work items
+// walk (prime, sub-block, batch), the staged tables are the sub-block's slices of
+// the large transform's tables (entry idx of the virtual table is entry
+// idx + ((2^log_s + g - 1) << floor(log2 idx)) of the real one), forward inputs
+// arrive lazily reduced (< 4p) and inverse outputs leave lazily reduced (< 2p,
+// N^-1 is merged by the outer pass).
+template <int LOGN, bool FWD, bool SUB = false>
 __global__ void __launch_bounds__(Geo<LOGN, 4>::NT, ntt32_minb<LOGN>())
     k_ntt32_b(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int64_t batch,
               int nprimes, int prime_base, const uint2* __restrict__ tw_all,
-              const Prime32Info* __restrict__ info, const uint32_t* __restrict__ twm_all) {
+              const Prime32Info* __restrict__ info, const uint32_t* __restrict__ twm_all,
+              int log_s = 0) {
   typedef Geo<LOGN, 4> G_;
   constexpr int E = G_::E;
   constexpr int NT = G_::NT;
@@ -183,14 +192,21 @@ __global__ void __launch_bounds__(Geo<LOGN, 4>::NT, ntt32_minb<LOGN>())
   uint64_t* mbar = reinterpret_cast<uint64_t*>(stage + N);
   uint32_t* twl = reinterpret_cast<uint32_t*>(mbar + 2);  // LASTSM: entries [NTW, N)
   const int tid = threadIdx.x;
-  const int64_t P = batch * nprimes;
+  const int nsub = SUB ? 1 << log_s : 1;
+  const int64_t P = batch * nprimes * nsub;
   const int64_t qbeg = P * blockIdx.x / gridDim.x;
   const int64_t qend = P * (blockIdx.x + 1) / gridDim.x;
   if (qbeg >= qend) return;
-  // prime-major work order q -> (prime j, batch index b); memory is (b, j, N)
+  // prime-major work order q -> (prime j, [sub-block g,] batch index b); memory is
+  // (b, j, N) (SUB: (b, j, g, N))
   auto poly = [&](int64_t q) {
-    const int64_t j = q / batch, b = q - j * batch;
-    return (b * nprimes + j) * (int64_t)N;
+    const int64_t jg = q / batch, b = q - jg * batch;
+    if constexpr (SUB) {
+      const int64_t j = jg >> log_s, g = jg - (j << log_s);
+      return ((b * nprimes + j) * nsub + g) * (int64_t)N;
+    } else {
+      return (b * nprimes + jg) * (int64_t)N;
+    }
   };
   if (tid == 0) {
     mbar_init(mbar, 1);
@@ -203,19 +219,31 @@ __global__ void __launch_bounds__(Geo<LOGN, 4>::NT, ntt32_minb<LOGN>())
   Prime32Info inf;
   const uint2* twg = nullptr;
   for (int64_t q = qbeg; q < qend; ++q) {
-    const int j = (int)(q / batch);
-    if (j != cur) {  // (re)stage this prime's full-pass twiddles
-      cur = j;
+    const int jg = (int)(q / batch);  // prime (SUB: prime * nsub + sub-block)
+    if (jg != cur) {  // (re)stage this prime's (sub-block's) twiddles
+      cur = jg;
+      const int j = SUB ? jg >> log_s : jg;
       inf = info[prime_base + j];
-      twg = tw_all + (size_t)(prime_base + j) * N;
-      __syncthreads();  // the previous prime's table is no longer read
-      const uint4* src = reinterpret_cast<const uint4*>(twg);
-      uint4* dst = reinterpret_cast<uint4*>(tws);
-      for (int i = tid; i < NTW / 2; i += NT) dst[i] = __ldg(src + i);
-      if constexpr (LASTSM) {
-        const uint4* srcm = reinterpret_cast<const uint4*>(twm_all + (size_t)(prime_base + j) * N + NTW);
-        uint4* dstm = reinterpret_cast<uint4*>(twl);
-        for (int i = tid; i < (N - NTW) / 4; i += NT) dstm[i] = __ldg(srcm + i);
+      twg = tw_all + (size_t)(prime_base + j) * (SUB ? (size_t)N << log_s : (size_t)N);
+      __syncthreads();  // the previous table is no longer read
+      if constexpr (SUB) {
+        static_assert(!SUB || LASTSM, "the sub-block form stages both table parts");
+        const uint32_t bm1 = (uint32_t)(nsub + (jg - (j << log_s)) - 1);  // base - 1
+        const uint32_t* twmg = twm_all + (size_t)(prime_base + j) * ((size_t)N << log_s);
+        for (int i = tid; i < NTW; i += NT)
+          tws[i] = __ldg(twg + (i ? i + (bm1 << (31 - __clz(i))) : 0));
+        for (int i = NTW + tid; i < N; i += NT)
+          twl[i - NTW] = __ldg(twmg + i + (bm1 << (31 - __clz(i))));
+      } else {
+        const uint4* src = reinterpret_cast<const uint4*>(twg);
+        uint4* dst = reinterpret_cast<uint4*>(tws);
+        for (int i = tid; i < NTW / 2; i += NT) dst[i] = __ldg(src + i);
+        if constexpr (LASTSM) {
+          const uint4* srcm =
+              reinterpret_cast<const uint4*>(twm_all + (size_t)(prime_base + j) * N + NTW);
+          uint4* dstm = reinterpret_cast<uint4*>(twl);
+          for (int i = tid; i < (N - NTW) / 4; i += NT) dstm[i] = __ldg(srcm + i);
+        }
       }
       __syncthreads();
     }
@@ -239,7 +267,7 @@ __global__ void __launch_bounds__(Geo<LOGN, 4>::NT, ntt32_minb<LOGN>())
       if (HEFV_DIAG & 16) {
 #pragma unroll
         for (int e = 0; e < E; ++e) x[e] = (uint32_t)(tid * 977 + e * 131 + (int)q);
-      } else if (inf.p >= (1u << 30)) {
+      } else if (SUB || inf.p >= (1u << 30)) {
 #pragma unroll
         for (int e = 0; e < E; ++e) x[e] = stage[tid + e * NT];
       } else if (inf.p > (1u << 29)) {
@@ -296,7 +324,8 @@ __global__ void __launch_bounds__(Geo<LOGN, 4>::NT, ntt32_minb<LOGN>())
       if constexpr (LASTSM) {
         const Mod32M mm{inf.p, 2 * inf.p, inf.pinv};
         inv_last_pass<LOGN, 4, Mod32M>(mm, x, tid, twl - NTW, 0u, 0u);  // N^-1 is in pass 0
-        cta_inv<LOGN, 4, Mod32, decltype(hook), false>(md, x, sm, tws, inf.ninv, inf.wn, twg, hook);
+        cta_inv<LOGN, 4, Mod32, decltype(hook), false, SUB>(md, x, sm, tws, inf.ninv, inf.wn, twg,
+                                                            hook);
       } else if constexpr (ALLSM) {
         cta_inv<LOGN, 4, Mod32>(md, x, sm, tws, inf.ninv, inf.wn, nullptr, hook);
       } else {
@@ -310,7 +339,7 @@ __global__ void __launch_bounds__(Geo<LOGN, 4>::NT, ntt32_minb<LOGN>())
       if (acc == 0x12345u) dst[tid] = acc;
 #else
 #pragma unroll
-      for (int e = 0; e < E; ++e) dst[tid + e * NT] = md.subp(x[e]);
+      for (int e = 0; e < E; ++e) dst[tid + e * NT] = SUB ? x[e] : md.subp(x[e]);
 #endif
     }
   }
@@ -650,7 +679,7 @@ static int launch_b32(bool fwd, const uint32_t* in, uint32_t* out, int64_t batch
   const int64_t P = batch * nprimes;
   const int64_t slots = (int64_t)sm_count() * per_sm;
   const unsigned grid = (unsigned)(P < slots ? P : slots);
-  kern<<<grid, G_::NT, smem, st>>>(in, out, batch, nprimes, prime_base, tw, info, twm);
+  kern<<<grid, G_::NT, smem, st>>>(in, out, batch, nprimes, prime_base, tw, info, twm, 0);
   HEFV_LAUNCH_CHECK("k_ntt32_b");
   return 0;
 }
@@ -682,6 +711,105 @@ static int launch_b64(bool fwd, const uint64_t* in, uint64_t* out, int64_t batch
   const unsigned grid = (unsigned)(P < slots ? P : slots);
   kern<<<grid, G_::NT, smem, st>>>(in, out, batch, nprimes, prime_base, tw, info, bcast);
   HEFV_LAUNCH_CHECK("k_ntt64_b");
+  return 0;
+}
+
+// ---- 30-bit transforms of 2^15 / 2^16 points as two HBM passes ---------------
+// The same split as the 64-bit one (k_ntt64_top / k_ntt64_sub): the S = LOGN - 14
+// outermost stages stream over HBM, the remaining 14 run as 2^S sub-transforms
+// in the persistent 2^14 kernel (k_ntt32_b<14, ., SUB>).  Replaces the
+// 1024-thread x 32-word single CTA at 2^15 (0.37 / 0.43 of the butterfly peak)
+// and the 4-CTA cluster at 2^16 (0.35 / 0.37) in device order.
+template <int S, bool FWD, class TIn>
+__global__ void __launch_bounds__(256)
+    k_ntt32_top(const TIn* __restrict__ in, uint32_t* __restrict__ out, int nprimes,
+                int prime_base, int log_n, const uint2* __restrict__ tw_all,
+                const Prime32Info* __restrict__ info, int bcast) {
+  constexpr int R = 1 << S;
+  const int64_t n = (int64_t)1 << log_n;
+  const int64_t ns = n >> S;
+  const int chunks = (int)(ns >> 8);
+  const int64_t q = blockIdx.x / chunks;  // polynomial (b, j), j fastest
+  const int64_t idx = (int64_t)(blockIdx.x - q * chunks) * 256 + threadIdx.x;
+  const int j = (int)(q % nprimes);
+  const Prime32Info inf = info[prime_base + j];
+  const Mod32 md{inf.p, 2 * inf.p};
+  const uint2* tw = tw_all + (size_t)(prime_base + j) * n;
+  uint32_t* dst = out + q * n + idx;
+  uint32_t x[R];
+  if constexpr (FWD) {
+    const TIn* src = in + (bcast ? q / nprimes : q) * n + idx;
+#pragma unroll
+    for (int e = 0; e < R; ++e) x[e] = cl_in(src[e * ns], inf);
+#pragma unroll
+    for (int l = 0; l < S; ++l) {
+      const int half = R >> (l + 1);
+#pragma unroll
+      for (int u = 0; u < (1 << l); ++u) {
+        const uint2 w = __ldg(tw + (1 << l) + u);
+#pragma unroll
+        for (int e0 = 0; e0 < half; ++e0) md.ct(x[u * 2 * half + e0], x[u * 2 * half + e0 + half], w);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < R; ++e) dst[e * ns] = x[e];  // lazy, < 4p
+  } else {
+#pragma unroll
+    for (int e = 0; e < R; ++e) x[e] = dst[e * ns];  // < 2p from the sub-transforms
+#pragma unroll
+    for (int l = S - 1; l >= 0; --l) {
+      const int half = R >> (l + 1);
+#pragma unroll
+      for (int u = 0; u < (1 << l); ++u) {
+        if (l == 0) {
+#pragma unroll
+          for (int e0 = 0; e0 < half; ++e0) md.gs_last(x[e0], x[e0 + half], inf.ninv, inf.wn);
+        } else {
+          const uint2 w = __ldg(tw + (1 << l) + u);
+#pragma unroll
+          for (int e0 = 0; e0 < half; ++e0) md.gs(x[u * 2 * half + e0], x[u * 2 * half + e0 + half], w);
+        }
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < R; ++e) dst[e * ns] = md.subp(x[e]);
+  }
+}
+
+// rows: polynomials per prime (bcast: input rows, each transformed under every prime)
+template <int S, class TIn>
+static int launch_split32(bool fwd, const TIn* in, uint32_t* out, int64_t rows, int nprimes,
+                          int prime_base, const uint2* tw, const Prime32Info* info,
+                          const uint32_t* twm, cudaStream_t st, int bcast) {
+  const int log_n = 14 + S;
+  const int64_t polys = rows * nprimes;
+  if (polys <= 0) return 0;
+  const int64_t top_blocks = polys << (log_n - S - 8);
+  if (top_blocks > 0x7fffffff) return fail("ntt32: batch too large");
+  const size_t smem = fwd ? Ntt32B<14, true>::smem : Ntt32B<14, false>::smem;
+  auto sub = fwd ? k_ntt32_b<14, true, true> : k_ntt32_b<14, false, true>;
+  HEFV_CUDA(cudaFuncSetAttribute(sub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t P = polys << S;
+  const int64_t slots = sm_count();
+  const unsigned grid = (unsigned)(P < slots ? P : slots);
+  if (fwd) {
+    k_ntt32_top<S, true, TIn><<<(unsigned)top_blocks, 256, 0, st>>>(in, out, nprimes, prime_base,
+                                                                     log_n, tw, info, bcast);
+    HEFV_LAUNCH_CHECK("k_ntt32_top");
+    sub<<<grid, 1024, smem, st>>>(out, out, rows, nprimes, prime_base, tw, info, twm, S);
+    HEFV_LAUNCH_CHECK("k_ntt32_b sub");
+  } else {
+    if constexpr (sizeof(TIn) != 4) {
+      return fail("ntt32: wide rows are a forward-only input form");
+    } else {
+      if (bcast) return fail("ntt32: broadcast rows are a forward-only input form");
+      sub<<<grid, 1024, smem, st>>>(in, out, rows, nprimes, prime_base, tw, info, twm, S);
+      HEFV_LAUNCH_CHECK("k_ntt32_b sub");
+      k_ntt32_top<S, false, uint32_t><<<(unsigned)top_blocks, 256, 0, st>>>(
+          out, out, nprimes, prime_base, log_n, tw, info, 0);
+      HEFV_LAUNCH_CHECK("k_ntt32_top");
+    }
+  }
   return 0;
 }
 
@@ -1139,8 +1267,9 @@ int hefv_ntt32_large(hefv_ctx* c, bool fwd, const uint32_t* in, uint32_t* out, i
                      int nprimes, int prime_base, int natural, cudaStream_t st) {
   if (c->log_n != 16) return fail("ntt32: unsupported ring dimension");
   if (natural) return fail("ntt32: N = 2^16 runs in device order only");
-  return launch_cl<16, Mod32, uint32_t>(fwd, in, out, batch * nprimes, nprimes, prime_base,
-                                        fwd ? c->d_tw32 : c->d_itw32, c->d_info32, st, 0);
+  return launch_split32<2, uint32_t>(fwd, in, out, batch, nprimes, prime_base,
+                                     fwd ? c->d_tw32 : c->d_itw32, c->d_info32,
+                                     fwd ? c->d_twm32 : c->d_itwm32, st, 0);
 }
 
 // Forward transforms (device order) of u64 rows (< 2^62) under the 32-bit
@@ -1169,12 +1298,12 @@ int hefv_ntt32_fwd_rows64(hefv_ctx* c, const uint64_t* in, uint32_t* out, int64_
     HEFV_R64(13)
     HEFV_R64(14)
 #undef HEFV_R64
-    case 15:
+    case 15:  // (the split form measured equal here: its outer pass is one stage per HBM trip)
       return launch_cl<15, Mod32, uint64_t>(true, in, out, total, nprimes, prime_base, c->d_tw32,
                                             c->d_info32, st, 1);
     case 16:
-      return launch_cl<16, Mod32, uint64_t>(true, in, out, total, nprimes, prime_base, c->d_tw32,
-                                            c->d_info32, st, 1);
+      return launch_split32<2, uint64_t>(true, in, out, rows, nprimes, prime_base, c->d_tw32,
+                                         c->d_info32, c->d_twm32, st, 1);
     default:
       return fail("ntt32_rows64: ring dimension outside 2^10..2^16");
   }
