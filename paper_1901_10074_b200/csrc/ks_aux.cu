@@ -51,11 +51,12 @@ namespace hefv {
 #define KSA_INV_CTS_V 16
 #endif
 #ifndef KSA_MAC_CTS_V
-#define KSA_MAC_CTS_V 128
+#define KSA_MAC_CTS_V 256
 #endif
 constexpr int KSA_FWD_CTS = KSA_FWD_CTS_V;  // ciphertexts per CTA, phase 1
 constexpr int KSA_INV_CTS = KSA_INV_CTS_V;  // ciphertexts per CTA, phase 3
-constexpr int KSA_MAC_CTS = KSA_MAC_CTS_V;  // ciphertexts per CTA, phase 2 (key tile reuse)
+constexpr int KSA_MAC_CTS = KSA_MAC_CTS_V;  // ciphertexts per CTA at most, phase 2 (key tile
+                                            // reuse; a launch's CTAs get equal shares)
 constexpr int KSA_KMAX = 24;     // digits held in registers by phase 2
 
 // "Tiled" point layout of a (k, N) stack: [N/32][k][32] -- the k values of a
@@ -308,8 +309,8 @@ __global__ void __launch_bounds__(32 * (JW + 1 + ksa_pw(JW)), 1)
   const int m = blockIdx.x - t * tiles;
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
-  const int64_t bbeg = (int64_t)blockIdx.y * KSA_MAC_CTS;
-  const int64_t bend = min(B, bbeg + KSA_MAC_CTS);
+  const int64_t bbeg = B * blockIdx.y / gridDim.y;  // equal shares of at most KSA_MAC_CTS
+  const int64_t bend = B * (blockIdx.y + 1) / gridDim.y;
   const int nb = (int)(bend - bbeg);
   const uint32_t full0 = smem_u32(&bars[0][0]), empty0 = smem_u32(&bars[1][0]);
   const uint32_t xready0 = smem_u32(&bars[2][0]), xempty0 = smem_u32(&bars[3][0]);
