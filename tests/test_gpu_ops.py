@@ -266,8 +266,8 @@ def test_ntt_golden_vectors(case):
 
 # ---------------------------------------------------------------- race stress
 @pytest.mark.parametrize("log_n,bits", [(10, 30), (12, 30), (13, 30), (14, 30), (15, 30),
-                                        (10, 50), (12, 50), (13, 60), (14, 55), (15, 55),
-                                        (16, 60)])
+                                        (16, 30), (10, 50), (12, 50), (13, 60), (14, 55),
+                                        (15, 55), (16, 60)])
 def test_transform_roundtrip_stress(log_n, bits):
     """Many CTAs, repeated: device-order forward then inverse must be the
     identity bit for bit (catches exchange/barrier races)."""
@@ -355,8 +355,9 @@ def test_ntt64_device_order_matches_oracle(log_n, bits):
 @pytest.mark.parametrize("log_n,bits", [(10, 30), (12, 30), (13, 30), (14, 30), (15, 30),
                                         (16, 30), (14, 28), (12, 24)])
 def test_ntt32_device_order_matches_oracle(log_n, bits):
-    """Batched 30-bit device-order transforms (the persistent k_ntt32_b /
-    cluster path, prime boundaries inside CTA ranges, inputs up to 2^32 - 1)
+    """Batched 30-bit device-order transforms (the persistent k_ntt32_b, the
+    32-word single CTA at 2^15 and the split outer-pass + sub-transform form at
+    2^16; prime boundaries inside CTA ranges, inputs up to 2^32 - 1)
     equal the oracle's natural-order NTT permuted into bit-reversed order,
     and invert to x mod p."""
     import ctypes as C
