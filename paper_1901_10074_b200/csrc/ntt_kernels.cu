@@ -101,7 +101,15 @@ __global__ void __launch_bounds__(Geo<LOGN, LOGE>::NT)
   const int tid = threadIdx.x;
   T x[G_::E];
   if (!natural) {
-    load_row_vec<LOGN, LOGE, T>(src, tid, x);
+    if constexpr (sizeof(T) == 8 && LOGE == 4 && G_::NT >= 32 && NTT64_ROWIO) {
+      uint4 c[8];  // warp-contiguous 128-bit loads (see k_ntt64_sub); the tile is unused yet
+      const uint4* s4 = reinterpret_cast<const uint4*>(src + (tid >> 5) * 512) + (tid & 31);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) c[i] = __ldg(s4 + 32 * i);
+      warp_chunks_to_rows64(warp_tile_region(sm, tid), tid & 31, c, x);
+    } else {
+      load_row_vec<LOGN, LOGE, T>(src, tid, x);
+    }
   } else {
 #pragma unroll
     for (int e = 0; e < G_::E; ++e)
@@ -437,7 +445,8 @@ __global__ void __launch_bounds__(Geo<LOGN, 4>::NT, LOGN >= 13 ? 1024 / Geo<LOGN
         store_row_vec<LOGN, 4, uint64_t>(dst, tid, x);
       }
     } else {
-      // (2^13: the chunk registers spill at 64 registers per thread, 0.659 -> 0.626)
+      // (2^13: the chunk registers spill at 64 registers per thread, 0.659 -> 0.626, and one
+      // 512-thread CTA per SM at 128 registers loses more: 0.745 / 0.660 -> 0.717 / 0.649)
       if constexpr (NTT64_ROWIO && LOGN == 14) {
         uint4 c[8];
         const uint4* s4 = reinterpret_cast<const uint4*>(src + (tid >> 5) * 512) + (tid & 31);
