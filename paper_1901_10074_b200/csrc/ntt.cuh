@@ -25,7 +25,10 @@
 #include "modarith.cuh"
 
 #ifndef HEFV_DIAG
-#define HEFV_DIAG 0  // timing diagnostics only (wrong results): 1 no exchange, 2 no group barriers
+// Timing diagnostics only (the results are wrong): 1 no shared-memory exchanges,
+// 2 no group barriers, 8 no output (k_ntt32_b), 16 no input (k_ntt32_b).  Built
+// with tools/build_variant.sh; they priced the parts of a transform.
+#define HEFV_DIAG 0
 #endif
 
 namespace hefv {
@@ -64,25 +67,6 @@ __device__ __forceinline__ int row_index(int tid, int e) {
 // twiddles with 16-byte accesses where possible.
 template <class Tw, int MAXC>
 __device__ __forceinline__ void load_tw_run(const Tw* __restrict__ p, Tw* out, const int count) {
-#if HEFV_DIAG & 4
-  if constexpr (sizeof(Tw) == 8) {
-#pragma unroll
-    for (int i = 0; i < MAXC; ++i) {
-      uint2 v = make_uint2(123456789u + 977u * i, 493903u + 13u * i);
-      asm volatile("" : "+r"(v.x), "+r"(v.y));
-      out[i] = *reinterpret_cast<Tw*>(&v);
-    }
-    return;
-  } else if constexpr (sizeof(Tw) == 4) {
-#pragma unroll
-    for (int i = 0; i < MAXC; ++i) {
-      uint32_t v = 123456789u + 977u * i;
-      asm volatile("" : "+r"(v));
-      out[i] = *reinterpret_cast<Tw*>(&v);
-    }
-    return;
-  }
-#endif
   if (sizeof(Tw) == 4 && count % 4 == 0) {  // single-word (Montgomery) twiddles
     const uint4* q = reinterpret_cast<const uint4*>(p);
 #pragma unroll
