@@ -219,6 +219,10 @@ constexpr int KSA_STAGES = KSA_STAGES_V;  // depth of the digit-tile ring
 // 24-consumer CTA of k = 23, 24 (config-3 hop 24.4 -> 23.7 us), one otherwise
 // (two measured slower at k = 22: 20.7 -> 21.2 us).
 __host__ __device__ constexpr int ksa_pw(int JW) { return JW > 22 ? 2 : 1; }
+#ifndef KSA_MAC_PLAIN
+#define KSA_MAC_PLAIN 0  // k >= 22 MAC: the first KSA_MAC_PLAIN digit pairs as a direct sum (2 IMAD.WIDE per
+                         // pair, no factor sums) instead of Winograd pair products (A/B; 99 = all)
+#endif
 #ifndef KSA_MAC_ALLSMEM
 #define KSA_MAC_ALLSMEM 0  // k = 22 MAC: body key pairs in shared memory too (A/B)
 #endif
@@ -351,7 +355,7 @@ __global__ void __launch_bounds__(32 * (JW + 1 + ksa_pw(JW)), 1)
 #pragma unroll
       for (int u = 0; u < H; ++u) {
         const uint32_t x0 = xt[64 * u], x1 = xt[64 * u + 32];
-        mad_wide((u & 1) ? p1 : p0, x0, x1);
+        if (JW < 22 || u >= KSA_MAC_PLAIN) mad_wide((u & 1) ? p1 : p0, x0, x1);
         xx[st][u][lane] = make_uint2(x0, x1);
       }
       xpair[st][lane] = p0 + p1;
@@ -401,8 +405,10 @@ __global__ void __launch_bounds__(32 * (JW + 1 + ksa_pw(JW)), 1)
         kb[u] = ((uint64_t)b0 << 32) | b1;
         kms[(u * JW + w) * 32 + lane] = ((uint64_t)m0 << 32) | m1;
       }
-      mad_wide(kpb, b0, b1);
-      mad_wide(kpm, m0, m1);
+      if (u >= KSA_MAC_PLAIN) {
+        mad_wide(kpb, b0, b1);
+        mad_wide(kpm, m0, m1);
+      }
     }
   }
   const uint64_t* kmw = kms + w * 32 + lane;
@@ -434,6 +440,18 @@ __global__ void __launch_bounds__(32 * (JW + 1 + ksa_pw(JW)), 1)
         kbu = kb[u];
         kmu = kmw[u * JW * 32];
       }
+      if (u < KSA_MAC_PLAIN) {
+        // direct sum: x_2u k_2u + x_2u+1 k_2u+1 (packed key = (k_2u : k_2u+1)); x, k < a < 2^28.1,
+        // so the accumulators stay inside the Winograd bound above
+        mad_wide(b0, xv0.x, (uint32_t)(kbu >> 32));
+        mad_wide(m0, xv0.x, (uint32_t)(kmu >> 32));
+        mad_wide(b1, xv1.x, (uint32_t)(kbu >> 32));
+        mad_wide(m1, xv1.x, (uint32_t)(kmu >> 32));
+        mad_wide(b0, xv0.y, (uint32_t)kbu);
+        mad_wide(m0, xv0.y, (uint32_t)kmu);
+        mad_wide(b1, xv1.y, (uint32_t)kbu);
+        mad_wide(m1, xv1.y, (uint32_t)kmu);
+      } else {
       const uint64_t xw0 = ((uint64_t)xv0.y << 32) | xv0.x;
       const uint64_t xw1 = ((uint64_t)xv1.y << 32) | xv1.x;
       const uint64_t sb0 = xw0 + kbu, sm0 = xw0 + kmu;
@@ -442,6 +460,7 @@ __global__ void __launch_bounds__(32 * (JW + 1 + ksa_pw(JW)), 1)
       mad_wide(m0, (uint32_t)sm0, (uint32_t)(sm0 >> 32));
       mad_wide(b1, (uint32_t)sb1, (uint32_t)(sb1 >> 32));
       mad_wide(m1, (uint32_t)sm1, (uint32_t)(sm1 >> 32));
+      }
     }
     const uint64_t xp0 = xpair[st0][lane];
     const uint64_t xp1 = two ? xpair[st1][lane] : 0ull;
